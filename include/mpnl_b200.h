@@ -1,0 +1,105 @@
+/*
+ * mpnl_b200 — C ABI of the B200-native MPNL parallel-path MIMO detector.
+ *
+ * Plain pointers and sizes only.  Device pointers are CUDA device memory
+ * (e.g. torch.Tensor.data_ptr()), `stream` is a cudaStream_t (0 = legacy).
+ * Every call returns 0 on success, a negative MPNL_E* code otherwise;
+ * mpnl_last_error() gives the message of the calling thread's last failure.
+ *
+ * Reference interfaces replaced (the Python package `mpnlsim`, detect.py):
+ *   mpnl_alloc_expansions  <- allocate_expansions   detect.py:221-280
+ *   mpnl_plan              <- mpnl_plan_batch / _sorted_qr_batch
+ *                                                    detect.py:321-388
+ *   mpnl_detect_hard       <- mpnl_detect_batch + take_along_axis(labels, best)
+ *                             (the hard-output composition of cli.py:236-239
+ *                              and test_acceptance.py:114-117)
+ *   mpnl_detect_full       <- mpnl_detect_batch      detect.py:473-488
+ * INTEGRATION.md shows the ctypes binding a maintainer adds to detect.py.
+ */
+#ifndef MPNL_B200_H
+#define MPNL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPNL_OK 0
+#define MPNL_EINVAL (-1)      /* invalid argument (reference: ValueError)      */
+#define MPNL_EUNSUPPORTED (-2) /* N > 32, M > 64, Q not in {4,16,64}          */
+#define MPNL_ECUDA (-3)       /* CUDA runtime error                            */
+
+/* Last error message of the calling thread ("" if none). */
+const char* mpnl_last_error(void);
+
+/* Library / ABI version, e.g. 0x000100 for 0.1.0. */
+int mpnl_version(void);
+
+/* Per-layer expansion counts (indexed by tree position, n_layers-1 = top) and
+ * the realized path count.  *warned = 1 when n_paths < q^n_forced (the
+ * reference's UserWarning).  Errors: n_paths < 1 -> MPNL_EINVAL
+ * ("n_paths must be >= 1").  Host function. */
+int mpnl_alloc_expansions(int n_layers, int q, int64_t n_paths, int n_forced,
+                          int64_t* expansions_out, int64_t* realized_out,
+                          int* warned);
+
+/* floats per channel of the fp32 traversal table blob. */
+int64_t mpnl_tables_floats(int m, int n);
+
+/* Plan n_ch channels h (n_ch, m, n) row-major complex64 (h_is_f64 = 0) or
+ * complex128 (1).  Augmented planning ([H; sqrt(nv) I]) when n > m.
+ * Outputs (device): perm (n_ch, n) int32, r64 (n_ch, n, n) complex128,
+ * qh64 (n_ch, n, m) complex128, tables (n_ch, mpnl_tables_floats) float32. */
+int mpnl_plan(const void* h, int h_is_f64, int64_t n_ch, int m, int n, int q,
+              double noise_var, int32_t* perm, void* r64, void* qh64,
+              float* tables, void* stream);
+
+/* Scratch bytes mpnl_detect_hard needs for n_vectors received vectors. */
+int64_t mpnl_workspace_bytes(int64_t n_vectors);
+
+/* Hard-output detection of y (n_ch, v_per_ch, m) (complex64 or complex128)
+ * against the plan: writes hard (n_ch*v_per_ch, n) uint8 point labels in
+ * stream order and metric (n_ch*v_per_ch) float32 = ||y - H x_hat||^2.
+ * expansions: host array of n int64 (from mpnl_alloc_expansions).
+ * flags (optional, may be NULL): 1 where the fp32 pass was re-done in fp64.
+ * Launches the fp32 traversal kernel, then the fp64 fix-up kernel. */
+int mpnl_detect_hard(const int32_t* perm, const void* r64, const void* qh64,
+                     const float* tables, const void* y, int y_is_f64,
+                     int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
+                     const int64_t* expansions, double noise_var,
+                     uint8_t* hard, float* metric, uint8_t* flags,
+                     void* workspace, int64_t workspace_bytes, void* stream);
+
+/* The two stages of mpnl_detect_hard, for timing: stage 1 = fp32 traversal
+ * (+ flag list), stage 2 = fp64 fix-up of the flagged vectors. */
+int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64,
+                           const void* qh64, const float* tables, const void* y,
+                           int y_is_f64, int64_t n_ch, int64_t v_per_ch, int m,
+                           int n, int q, const int64_t* expansions,
+                           double noise_var, uint8_t* hard, float* metric,
+                           uint8_t* flags, void* workspace,
+                           int64_t workspace_bytes, void* stream);
+
+/* Full candidate list (reference-compatible mpnl_detect_batch), fp64:
+ * labels (B, P, n) uint8 in path order and stream order, metrics (B, P)
+ * float64, best (B,) int64, B = n_ch * v_per_ch, P = prod(expansions). */
+int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64,
+                     const void* y, int y_is_f64, int64_t n_ch,
+                     int64_t v_per_ch, int m, int n, int q,
+                     const int64_t* expansions, double noise_var,
+                     uint8_t* labels, double* metrics, int64_t* best,
+                     void* stream);
+
+/* Guard scale c in tau = c * 2^-24 (default 2(m+n)+16 when c <= 0). */
+void mpnl_set_guard_scale(double c);
+
+/* FFMA throughput probe (for the roofline denominator): runs `iters` dependent
+ * FFMA chains on every SM; returns FLOPs executed.  out: device float[blocks*threads]. */
+int64_t mpnl_ffma_probe(float* out, int blocks, int threads, int iters, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPNL_B200_H */

@@ -1,0 +1,404 @@
+// C ABI of the MPNL B200 library (declared in include/mpnl_b200.h).
+//
+// Host side: argument validation with the reference's error behaviour, the
+// integer expansion allocator (C++ port of detect.py:221-280), the tree /
+// chunking parameters, and the kernel launches.  No host synchronisation,
+// no hidden allocations: scratch comes from the caller's workspace.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mpnl_b200.h"
+#include "common.cuh"
+#include "traverse.cuh"
+
+namespace mpnl {
+cudaError_t launch_plan(const void* h, int h_is_f64, int64_t n_ch, int m, int n, int L,
+                        double noise_var, int augmented, int32_t* perm, double2* r64,
+                        double2* qh64, float* tables, cudaStream_t st);
+#define MPNL_DECL_PART(LL, PP)                                                             \
+  cudaError_t launch_traverse_l##LL##_p##PP(int n, const TraverseArgs& a, const TreeParams& tp, \
+                                            int threads, unsigned grid, size_t smem,       \
+                                            cudaStream_t st);
+MPNL_DECL_PART(2, 0) MPNL_DECL_PART(2, 1) MPNL_DECL_PART(2, 2) MPNL_DECL_PART(2, 3)
+MPNL_DECL_PART(4, 0) MPNL_DECL_PART(4, 1) MPNL_DECL_PART(4, 2) MPNL_DECL_PART(4, 3)
+MPNL_DECL_PART(8, 0) MPNL_DECL_PART(8, 1) MPNL_DECL_PART(8, 2) MPNL_DECL_PART(8, 3)
+#undef MPNL_DECL_PART
+}  // namespace mpnl
+
+#include "exact_args.cuh"
+
+namespace mpnl {
+cudaError_t launch_exact(const ExactArgs& a, const TreeParams& tp, int grid, cudaStream_t st);
+}
+
+using namespace mpnl;
+
+namespace {
+
+thread_local std::string g_err;
+double g_guard_scale = 0.0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(MPNL_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int levels_for(int q) { return q == 4 ? 2 : (q == 16 ? 4 : (q == 64 ? 8 : 0)); }
+
+// detect.py:240-251 — greedy non-increasing factorisation of `budget`
+bool split_budget(int64_t budget, int slots, int64_t cap, std::vector<int64_t>& out) {
+  if (budget == 1) return true;
+  if (slots == 0) return false;
+  for (int64_t d = std::min(cap, budget); d >= 2; --d) {
+    if (budget % d) continue;
+    out.push_back(d);
+    if (split_budget(budget / d, slots - 1, d, out)) return true;
+    out.pop_back();
+  }
+  return false;
+}
+
+int64_t ipow_sat(int64_t b, int e, int64_t cap) {
+  int64_t r = 1;
+  for (int i = 0; i < e; ++i) {
+    if (r > cap / b) return cap + 1;
+    r *= b;
+  }
+  return r;
+}
+
+struct TreeBuild {
+  TreeParams tp;
+  bool ok;
+  std::string err;
+};
+
+TreeBuild build_tree(int n, int L, const int64_t* ex) {
+  TreeBuild b;
+  std::memset(&b.tp, 0, sizeof(b.tp));
+  b.ok = false;
+  const int q = L * L;
+  int64_t stride = 1;
+  b.tp.stride[0] = 1;
+  for (int pos = 0; pos < n; ++pos) {
+    if (ex[pos] < 1 || ex[pos] > q) { b.err = "expansions out of range [1, q]"; return b; }
+    b.tp.e[pos] = (int)ex[pos];
+    stride *= ex[pos];
+    if (stride > (1 << 24)) { b.err = "path budget too large (> 2^24)"; return b; }
+    b.tp.stride[pos + 1] = (int)stride;
+  }
+  b.tp.n_paths = (int)stride;
+  int ntop = 0;
+  for (int pos = n - 1; pos >= 0 && b.tp.e[pos] > 1; --pos) ++ntop;
+  for (int pos = n - 1 - ntop; pos >= 0; --pos)
+    if (b.tp.e[pos] != 1) { b.err = "expansions must be non-increasing from the top layer"; return b; }
+  b.tp.n_top = ntop;
+  int off = 0;
+  for (int pos = n - 1; pos >= n - ntop; --pos) {
+    const int e = b.tp.e[pos];
+    if (e < q) {
+      b.tp.list_off[pos] = off;
+      off += b.tp.n_paths / b.tp.stride[pos];
+      int cnt = 0;
+      for (int i = 0; i < L; ++i)
+        for (int j = 0; j < L; ++j)
+          if ((i + 1) * (j + 1) <= e + 1) ++cnt;
+      b.tp.stair_cnt[pos] = cnt;
+    }
+  }
+  b.tp.list_bytes = off;
+  b.ok = true;
+  return b;
+}
+
+int check_dims(int m, int n, int q) {
+  if (n < 1 || m < 1) return fail(MPNL_EINVAL, "inconsistent channel/observation dimensions");
+  if (n > MPNL_MAX_N) return fail(MPNL_EUNSUPPORTED, "N > 32 streams is not supported");
+  if (m > MPNL_MAX_M || (n > m && m + n > MPNL_MAX_M))
+    return fail(MPNL_EUNSUPPORTED, "M (or M+N when augmented) > 64 is not supported");
+  if (!levels_for(q)) return fail(MPNL_EUNSUPPORTED, "unsupported constellation order " + std::to_string(q));
+  return MPNL_OK;
+}
+
+struct Launch {
+  TraverseArgs a;
+  int threads;
+  unsigned grid;
+  size_t smem;
+};
+
+int trav_pt(int n) {
+  switch ((n + 7) / 8) {
+    case 1: return TravCfg<8>::PT;
+    case 2: return TravCfg<16>::PT;
+    case 3: return TravCfg<24>::PT;
+    default: return TravCfg<32>::PT;
+  }
+}
+int trav_maxt(int n) { return n <= 16 ? TravCfg<16>::MAXT : TravCfg<32>::MAXT; }
+
+cudaError_t launch_traverse(int n, int L, const Launch& l, const TreeParams& tp, cudaStream_t st) {
+  const int part = (n - 1) / 8;
+#define MPNL_PART(LL)                                                                    \
+  switch (part) {                                                                        \
+    case 0: return launch_traverse_l##LL##_p0(n, l.a, tp, l.threads, l.grid, l.smem, st); \
+    case 1: return launch_traverse_l##LL##_p1(n, l.a, tp, l.threads, l.grid, l.smem, st); \
+    case 2: return launch_traverse_l##LL##_p2(n, l.a, tp, l.threads, l.grid, l.smem, st); \
+    default: return launch_traverse_l##LL##_p3(n, l.a, tp, l.threads, l.grid, l.smem, st); \
+  }
+  if (L == 2) { MPNL_PART(2) }
+  if (L == 4) { MPNL_PART(4) }
+  MPNL_PART(8)
+#undef MPNL_PART
+}
+
+// Work decomposition of one channel's V vectors into CTA chunks (see
+// traverse.cuh phase C): VPI mode packs S/P vectors per warp item when P
+// divides S = 32*PT, batch mode loops ceil(P/S) slot batches per vector.
+bool plan_launch(int n, int m, int L, int64_t n_ch, int64_t V, const TreeParams& tp, Launch& l,
+                 std::string& err) {
+  const int pt = trav_pt(n), S = 32 * pt, P = tp.n_paths;
+  int vpi = 1, bpv = 1;
+  if (P < S && S % P == 0) vpi = S / P;
+  else bpv = (P + S - 1) / S;
+  const int maxt = trav_maxt(n);
+  const int warps = maxt / 32;
+  const int64_t items_ch = (V + vpi - 1) / vpi;
+  // items per CTA: a multiple of the warp count, ~4096 path slots per warp pass
+  int64_t per_warp = std::max<int64_t>(1, 4096 / ((int64_t)S * bpv * warps));
+  int64_t ipc = std::min<int64_t>(items_ch, warps * per_warp);
+  int vc = (int)std::min<int64_t>(V, ipc * vpi);
+  const int ngroups = maxt / MPNL_GROUP;
+  while (vc > 1 && TravSmem(m, n, vc, tp.list_bytes, ngroups).total_bytes > 200 * 1024) vc = (vc + 1) / 2;
+  const TravSmem so(m, n, vc, tp.list_bytes, ngroups);
+  if (so.total_bytes > 220 * 1024) { err = "shared-memory plan exceeds 220 KB"; return false; }
+  const int64_t chunks = (V + vc - 1) / vc;
+  if (n_ch * chunks > 0x7fffffffLL) { err = "grid too large"; return false; }
+  std::memset(&l.a, 0, sizeof(l.a));
+  l.a.V = V;
+  l.a.n_ch = n_ch;
+  l.a.m = m;
+  l.a.vc = vc;
+  l.a.chunks = (int)chunks;
+  l.a.vpi = vpi;
+  l.a.bpv = bpv;
+  int has_partial = 0;
+  for (int pos = n - 1; pos >= n - tp.n_top; --pos) has_partial |= tp.e[pos] < L * L;
+  l.a.has_partial = has_partial;
+  l.a.metric_offset = m > n;
+  const double cg = g_guard_scale > 0 ? g_guard_scale : 2.0 * (m + n) + 16.0;
+  l.a.tau = (float)(cg * std::ldexp(1.0, -24));
+  l.threads = maxt;
+  l.grid = (unsigned)(n_ch * chunks);
+  l.smem = so.total_bytes;
+  return true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* mpnl_last_error(void) { return g_err.c_str(); }
+
+int mpnl_version(void) { return 0x000100; }
+
+void mpnl_set_guard_scale(double c) { g_guard_scale = c; }
+
+int mpnl_alloc_expansions(int n_layers, int q, int64_t n_paths, int n_forced,
+                          int64_t* expansions_out, int64_t* realized_out, int* warned) {
+  if (n_paths < 1) return fail(MPNL_EINVAL, "n_paths must be >= 1");
+  if (n_layers < 1 || q < 2) return fail(MPNL_EINVAL, "n_layers must be >= 1 and q >= 2");
+  const int64_t cap = int64_t(1) << 40;
+  const int64_t full = ipow_sat(q, n_layers, cap);
+  if (full <= cap) n_paths = std::min(n_paths, full);
+  if (warned) *warned = 0;
+  if (n_forced > 0) {
+    const int64_t qf = ipow_sat(q, n_forced, cap);
+    if (n_paths < qf && warned) *warned = 1;
+  }
+  const int forced = std::min(n_forced, n_layers);
+  for (int64_t target = n_paths; target >= 1; --target) {
+    std::vector<int64_t> fac;
+    int64_t budget = target;
+    bool ok = true;
+    for (int i = 0; i < forced; ++i) {
+      if (budget >= q && budget % q == 0) { fac.push_back(q); budget /= q; }
+      else if (budget >= q) { ok = false; break; }
+      else { fac.push_back(budget); budget = 1; }
+    }
+    if (!ok) continue;
+    std::vector<int64_t> rest;
+    const int64_t cap0 = std::min<int64_t>(q, fac.empty() ? q : fac.back());
+    if (!split_budget(budget, n_layers - forced, cap0, rest)) continue;
+    fac.insert(fac.end(), rest.begin(), rest.end());
+    while ((int)fac.size() < n_layers) fac.push_back(1);
+    std::sort(fac.begin(), fac.end(), [](int64_t x, int64_t y) { return x > y; });
+    for (int i = 0; i < n_layers; ++i) expansions_out[n_layers - 1 - i] = fac[i];
+    *realized_out = target;
+    return MPNL_OK;
+  }
+  return fail(MPNL_EINVAL, "unreachable: no representable path budget");
+}
+
+int64_t mpnl_tables_floats(int m, int n) { return TableLayout(m, n).total; }
+
+int64_t mpnl_workspace_bytes(int64_t n_vectors) { return 16 + 8 * std::max<int64_t>(n_vectors, 1); }
+
+int mpnl_plan(const void* h, int h_is_f64, int64_t n_ch, int m, int n, int q, double noise_var,
+              int32_t* perm, void* r64, void* qh64, float* tables, void* stream) {
+  if (int rc = check_dims(m, n, q)) return rc;
+  if (n_ch < 0) return fail(MPNL_EINVAL, "negative batch");
+  if (n > m && !(noise_var > 0)) return fail(MPNL_EINVAL, "noise_var must be positive");
+  cudaError_t e = launch_plan(h, h_is_f64, n_ch, m, n, levels_for(q), noise_var, n > m ? 1 : 0,
+                              perm, (double2*)r64, (double2*)qh64, tables, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "plan kernel");
+  return MPNL_OK;
+}
+
+int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, const void* qh64,
+                           const float* tables, const void* y, int y_is_f64, int64_t n_ch,
+                           int64_t v_per_ch, int m, int n, int q, const int64_t* expansions,
+                           double noise_var, uint8_t* hard, float* metric, uint8_t* flags,
+                           void* workspace, int64_t workspace_bytes, void* stream) {
+  if (int rc = check_dims(m, n, q)) return rc;
+  const int L = levels_for(q);
+  const int64_t B = n_ch * v_per_ch;
+  if (n_ch < 0 || v_per_ch < 0) return fail(MPNL_EINVAL, "negative batch");
+  if (B == 0) return MPNL_OK;
+  if (workspace_bytes < mpnl_workspace_bytes(B)) return fail(MPNL_EINVAL, "workspace too small");
+  TreeBuild tb = build_tree(n, L, expansions);
+  if (!tb.ok) return fail(MPNL_EINVAL, tb.err);
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* count = reinterpret_cast<int32_t*>(workspace);
+  int64_t* list = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(workspace) + 16);
+  const bool augmented = n > m;
+  if (stage == 1) {
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return cuda_fail(e, "memset");
+    if (augmented) return MPNL_OK;   // overloaded channels: all vectors go to the fp64 kernel
+    Launch l;
+    std::string err;
+    if (!plan_launch(n, m, L, n_ch, v_per_ch, tb.tp, l, err)) return fail(MPNL_EUNSUPPORTED, err);
+    l.a.tables = tables;
+    l.a.y = y;
+    l.a.y_f64 = y_is_f64;
+    l.a.perm = perm;
+    l.a.hard = hard;
+    l.a.metric = metric;
+    l.a.flags = flags;
+    l.a.flag_count = count;
+    l.a.flag_list = list;
+    e = launch_traverse(n, L, l, tb.tp, st);
+    if (e != cudaSuccess) return cuda_fail(e, "traverse kernel");
+    return MPNL_OK;
+  }
+  ExactArgs ea;
+  std::memset(&ea, 0, sizeof(ea));
+  ea.r64 = (const double2*)r64;
+  ea.qh64 = (const double2*)qh64;
+  ea.perm = perm;
+  ea.y = y;
+  ea.y_f64 = y_is_f64;
+  ea.n_ch = n_ch;
+  ea.V = v_per_ch;
+  ea.m = m;
+  ea.n = n;
+  ea.L = L;
+  ea.noise_var = noise_var;
+  ea.augmented = augmented;
+  ea.hard = hard;
+  ea.metric = metric;
+  int grid;
+  if (augmented) {
+    ea.list = nullptr;
+    ea.n_tasks = B;
+    grid = (int)std::min<int64_t>((B + 3) / 4, 148 * 16);
+    if (flags) cudaMemsetAsync(flags, 1, B, st);
+  } else {
+    ea.list = list;
+    ea.count = count;
+    grid = (int)std::min<int64_t>((B + 3) / 4, 148 * 4);
+  }
+  cudaError_t e = launch_exact(ea, tb.tp, grid, st);
+  if (e != cudaSuccess) return cuda_fail(e, "exact kernel");
+  return MPNL_OK;
+}
+
+int mpnl_detect_hard(const int32_t* perm, const void* r64, const void* qh64, const float* tables,
+                     const void* y, int y_is_f64, int64_t n_ch, int64_t v_per_ch, int m, int n,
+                     int q, const int64_t* expansions, double noise_var, uint8_t* hard,
+                     float* metric, uint8_t* flags, void* workspace, int64_t workspace_bytes,
+                     void* stream) {
+  int rc = mpnl_detect_hard_stage(1, perm, r64, qh64, tables, y, y_is_f64, n_ch, v_per_ch, m, n,
+                                  q, expansions, noise_var, hard, metric, flags, workspace,
+                                  workspace_bytes, stream);
+  if (rc) return rc;
+  return mpnl_detect_hard_stage(2, perm, r64, qh64, tables, y, y_is_f64, n_ch, v_per_ch, m, n, q,
+                                expansions, noise_var, hard, metric, flags, workspace,
+                                workspace_bytes, stream);
+}
+
+int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64, const void* y,
+                     int y_is_f64, int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
+                     const int64_t* expansions, double noise_var, uint8_t* labels,
+                     double* metrics, int64_t* best, void* stream) {
+  if (int rc = check_dims(m, n, q)) return rc;
+  const int L = levels_for(q);
+  const int64_t B = n_ch * v_per_ch;
+  if (B == 0) return MPNL_OK;
+  TreeBuild tb = build_tree(n, L, expansions);
+  if (!tb.ok) return fail(MPNL_EINVAL, tb.err);
+  ExactArgs ea;
+  std::memset(&ea, 0, sizeof(ea));
+  ea.r64 = (const double2*)r64;
+  ea.qh64 = (const double2*)qh64;
+  ea.perm = perm;
+  ea.y = y;
+  ea.y_f64 = y_is_f64;
+  ea.n_ch = n_ch;
+  ea.V = v_per_ch;
+  ea.m = m;
+  ea.n = n;
+  ea.L = L;
+  ea.noise_var = noise_var;
+  ea.augmented = n > m;
+  ea.n_tasks = B;
+  ea.full_labels = labels;
+  ea.full_metrics = metrics;
+  ea.full_best = best;
+  ea.exact_order = 1;
+  const int grid = (int)std::min<int64_t>((B + 3) / 4, 148 * 16);
+  cudaError_t e = launch_exact(ea, tb.tp, grid, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "exact kernel");
+  return MPNL_OK;
+}
+
+}  // extern "C"
+
+// ---- FFMA throughput probe (roofline denominator) ----
+__global__ void ffma_probe_kernel(float* out, int iters) {
+  float x0 = threadIdx.x * 1e-3f, x1 = x0 + 1.f, x2 = x0 + 2.f, x3 = x0 + 3.f;
+  float x4 = x0 + 4.f, x5 = x0 + 5.f, x6 = x0 + 6.f, x7 = x0 + 7.f;
+  const float a = 0.999999f, b = 1e-7f;
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i) {
+    x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+    x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+extern "C" int64_t mpnl_ffma_probe(float* out, int blocks, int threads, int iters, void* stream) {
+  ffma_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(out, iters);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  return (int64_t)blocks * threads * iters * 8 * 2;
+}

@@ -1,0 +1,197 @@
+// K5 — fp64 parallel-path detector with the reference's exact decision rules.
+//
+// Two uses:
+//   * fix-up of the vectors the fp32 kernel flagged (near-boundary decisions
+//     on competitive paths, near-ties): recomputed here, results overwritten;
+//   * the reference-compatible full candidate list of `mpnl_detect_batch`
+//     (`/root/reference/pkg/src/mpnlsim/detect.py:473-488`): labels (B,P,N) in
+//     path order, metrics (B,P), best (B,).
+//
+// Semantics followed (detect.py):
+//   centre = (z_pos - acc_pos) / Re r_pp                         :417
+//   children = stable argsort(|centre - s_q|^2)[:e]              :418-419
+//     (ties -> lower point label; e = 1 is the 2-D nearest point, found
+//      per axis for square QAM with the same tie rule)
+//   path index mixed radix, top layer most significant           :420-422
+//   metric: true residual; computed here as the fp64 PED plus
+//     ||y||^2 - ||z||^2 (M > N) minus nv ||x||^2 (augmented)      :484-486
+//   best = lexicographic (metric, labels[stream 0], labels[1], ...) :465-470
+// One warp per received vector, lane = path (batches of 32 paths); per-lane
+// accumulators live in shared memory (runtime N, M).
+#include <math_constants.h>
+
+#include "exact_args.cuh"
+
+namespace mpnl {
+
+__device__ inline double lvl(int i, int L, double nrm) { return (double)(L - 1 - 2 * i) / nrm; }
+
+// lexicographic compare of two label rows (stream 0 most significant): a < b
+__device__ inline bool lab_less(const uint8_t* a, const uint8_t* b, int n) {
+  for (int i = 0; i < n; ++i)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return false;
+}
+
+__global__ void __launch_bounds__(32 * EX_WARPS)
+exact_kernel(const ExactArgs a, const TreeParams tp) {
+  extern __shared__ __align__(16) uint8_t exsm[];
+  const int n = a.n, m = a.m, L = a.L, Q = L * L;
+  const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
+  const double nrm = qam_norm_d(L);
+  const ExSmem so(n);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wsm = exsm + warp * so.total;
+  double2* acc = reinterpret_cast<double2*>(wsm + so.acc);   // [k][lane]
+  double2* zs = reinterpret_cast<double2*>(wsm + so.z);
+  uint8_t* lab = wsm + so.lab + lane * 32;
+  const int64_t ntask = a.list ? (int64_t)(*a.count) : a.n_tasks;
+  const int64_t gw = (int64_t)blockIdx.x * EX_WARPS + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * EX_WARPS;
+  const int P = tp.n_paths;
+
+  for (int64_t task = gw; task < ntask; task += nwarps) {
+    const int64_t gv = a.list ? a.list[task] : task;
+    const int64_t c = gv / a.V;
+    const double2* R = a.r64 + c * (int64_t)n * n;
+    const double2* QH = a.qh64 + c * (int64_t)n * m;
+    const int32_t* pc = a.perm + c * n;
+    // z = Q^H y (fp64), ||y||^2, ||z||^2
+    double yn = 0.0;
+    for (int r = 0; r < m; ++r) {
+      double yr, yi;
+      if (a.y_f64) {
+        const double2 v = reinterpret_cast<const double2*>(a.y)[gv * m + r];
+        yr = v.x; yi = v.y;
+      } else {
+        const float2 v = reinterpret_cast<const float2*>(a.y)[gv * m + r];
+        yr = v.x; yi = v.y;
+      }
+      yn = fma(yr, yr, fma(yi, yi, yn));
+      if (lane < n) {
+        const double2 q = QH[lane * m + r];
+        double2 z = r ? zs[lane] : make_double2(0.0, 0.0);
+        z.x = fma(q.x, yr, fma(-q.y, yi, z.x));
+        z.y = fma(q.x, yi, fma(q.y, yr, z.y));
+        zs[lane] = z;
+      }
+    }
+    __syncwarp();
+    double zn = 0.0;
+    for (int k = 0; k < n; ++k) zn = fma(zs[k].x, zs[k].x, fma(zs[k].y, zs[k].y, zn));
+    const double c0 = (m != n) ? (yn - zn) : 0.0;
+
+    double bm = CUDART_INF;   // lane-local best
+    int bp = 0x7fffffff;
+    const int nb = (P + 31) / 32;
+    for (int b = 0; b < nb; ++b) {
+      const int p = b * 32 + lane;
+      const bool ok = p < P;
+      for (int k = 0; k < n; ++k) acc[k * 32 + lane] = make_double2(0.0, 0.0);
+      double ped = 0.0, xs2 = 0.0;
+      for (int pos = n - 1; pos >= 0; --pos) {
+        const double rpp = R[pos * n + pos].x;
+        const double2 ap = acc[pos * 32 + lane];
+        const double ur = zs[pos].x - ap.x, ui = zs[pos].y - ap.y;
+        const double cr = ur / rpp, ci = ui / rpp;
+        const int e = tp.e[pos];
+        int ir = 0, ii = 0;
+        if (e == 1) {
+          double bd = CUDART_INF;
+          int bg = 1 << 30;
+          for (int i = 0; i < L; ++i) {
+            const double d = (cr - lvl(i, L, nrm)) * (cr - lvl(i, L, nrm));
+            const int g = gray_code(i);
+            if (d < bd || (d == bd && g < bg)) { bd = d; bg = g; ir = i; }
+          }
+          bd = CUDART_INF; bg = 1 << 30;
+          for (int i = 0; i < L; ++i) {
+            const double d = (ci - lvl(i, L, nrm)) * (ci - lvl(i, L, nrm));
+            const int g = gray_code(i);
+            if (d < bd || (d == bd && g < bg)) { bd = d; bg = g; ii = i; }
+          }
+        } else {
+          const int d = (p / tp.stride[pos]) % e;
+          if (e == Q && !a.exact_order) {
+            ir = d / L; ii = d % L;
+          } else {
+            // d-th point in stable (distance, label) order
+            double pd = -1.0;
+            int pl = -1;
+            for (int rnk = 0; rnk <= d; ++rnk) {
+              double bd = CUDART_INF;
+              int bl = 1 << 30, bq = 0;
+              for (int q = 0; q < Q; ++q) {
+                const int i = q / L, j = q % L;
+                const double dr = cr - lvl(i, L, nrm), di = ci - lvl(j, L, nrm);
+                const double dd = dr * dr + di * di;
+                const int lb = (gray_code(i) << h) | gray_code(j);
+                const bool after = dd > pd || (dd == pd && lb > pl);
+                const bool better = dd < bd || (dd == bd && lb < bl);
+                if (after && better) { bd = dd; bl = lb; bq = q; }
+              }
+              pd = bd; pl = bl;
+              ir = bq / L; ii = bq % L;
+            }
+          }
+        }
+        const double sr = lvl(ir, L, nrm), si = lvl(ii, L, nrm);
+        const double er = ur - rpp * sr, ei = ui - rpp * si;
+        ped = fma(er, er, fma(ei, ei, ped));
+        xs2 = fma(sr, sr, fma(si, si, xs2));
+        lab[pc[pos]] = (uint8_t)((gray_code(ir) << h) | gray_code(ii));
+        for (int k = 0; k < pos; ++k) {
+          const double2 r = R[k * n + pos];
+          double2 v = acc[k * 32 + lane];
+          v.x = fma(r.x, sr, fma(-r.y, si, v.x));
+          v.y = fma(r.x, si, fma(r.y, sr, v.y));
+          acc[k * 32 + lane] = v;
+        }
+      }
+      double met = ped + c0;
+      if (a.augmented) met -= a.noise_var * xs2;
+      if (ok && a.full_labels) {
+        uint8_t* fl = a.full_labels + (gv * P + p) * n;
+        for (int k = 0; k < n; ++k) fl[k] = lab[k];
+        a.full_metrics[gv * P + p] = met;
+      }
+      // lane-local best update with lexicographic tie-break
+      if (ok && (met < bm || (met == bm && lab_less(lab, wsm + so.blab + lane * 32, n)))) {
+        bm = met; bp = p;
+        for (int k = 0; k < n; ++k) wsm[so.blab + lane * 32 + k] = lab[k];
+      }
+    }
+    __syncwarp();
+    // warp argmin on (metric, labels)
+    int bl = lane;
+    for (int o = 16; o; o >>= 1) {
+      const double om = __shfl_xor_sync(0xffffffffu, bm, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      bool take = om < bm;
+      if (om == bm && op != 0x7fffffff && bp != 0x7fffffff)
+        take = lab_less(wsm + so.blab + ol * 32, wsm + so.blab + bl * 32, n);
+      if (om == bm && bp == 0x7fffffff && op != 0x7fffffff) take = true;
+      if (take) { bm = om; bl = ol; bp = op; }
+    }
+    if (lane == 0) {
+      const uint8_t* wl = wsm + so.blab + bl * 32;
+      if (a.hard)
+        for (int k = 0; k < n; ++k) a.hard[gv * n + k] = wl[k];
+      if (a.metric) a.metric[gv] = (float)bm;
+      if (a.metric64) a.metric64[gv] = bm;
+      if (a.full_best) a.full_best[gv] = bp;
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_exact(const ExactArgs& a, const TreeParams& tp, int grid, cudaStream_t st) {
+  const ExSmem so(a.n);
+  const size_t smem = (size_t)so.total * EX_WARPS;
+  cudaFuncSetAttribute(exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  exact_kernel<<<grid, 32 * EX_WARPS, smem, st>>>(a, tp);
+  return cudaGetLastError();
+}
+
+}  // namespace mpnl

@@ -1,0 +1,222 @@
+// K1 — per-channel planning: fp64 sorted (column-pivoted) complex QR and the
+// fp32 traversal tables.
+//
+// Follows the reference planner `mpnl_plan_batch` / `_sorted_qr_batch`
+// (`/root/reference/pkg/src/mpnlsim/detect.py:321-388`):
+//   * right-looking modified Gram-Schmidt on A = H, or [H; sqrt(nv) I] when
+//     N > M (detect.py:373-381);
+//   * pivot = first argmax (in current column order) of the *downdated* norms
+//     max(norm_j - |r_kj|^2, 0) (detect.py:335, 357);
+//   * r_kk recomputed from the pivot column, floored at 1e-300 (348-350);
+//   * Q^H = top M rows of Q, conjugate-transposed (383).
+//
+// B200 mapping: one warp per channel, lane j owns *physical* column j of A in
+// shared memory (A[m][j], lane-contiguous, conflict-free).  Column swaps are
+// pure bookkeeping (each lane tracks the logical position of its column), so
+// no data moves.  Row reductions (r_kk) are warp reductions over rows.
+// Everything is fp64; the fast path's fp32 tables are derived at the end.
+#include "common.cuh"
+
+namespace mpnl {
+
+template <typename TIn>
+__device__ inline double2 load_c(const TIn* p, int64_t i);
+template <>
+__device__ inline double2 load_c<float2>(const float2* p, int64_t i) {
+  float2 v = p[i];
+  return make_double2(v.x, v.y);
+}
+template <>
+__device__ inline double2 load_c<double2>(const double2* p, int64_t i) {
+  return p[i];
+}
+
+__device__ inline double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename TIn>
+__global__ void __launch_bounds__(32)
+plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
+               double noise_var, int augmented, int32_t* __restrict__ perm_out,
+               double2* __restrict__ r_out, double2* __restrict__ qh_out,
+               float* __restrict__ tables) {
+  extern __shared__ double2 smem[];
+  const int ma = augmented ? m + n : m;
+  double2* A = smem;              // [ma][n] physical columns
+  double2* Rp = smem + ma * n;    // [n][n] rows of R by physical column
+  const int64_t c = blockIdx.x;
+  if (c >= n_ch) return;
+  const int lane = threadIdx.x;
+
+  // ---- load A (row-parallel, coalesced over the (m, n) row-major input) ----
+  const TIn* hc = h + c * (int64_t)m * n;
+  for (int idx = lane; idx < m * n; idx += 32) A[idx] = load_c<TIn>(hc, idx);
+  if (augmented) {
+    const double s = sqrt(noise_var);
+    for (int idx = lane; idx < n * n; idx += 32) {
+      int i = idx / n, j = idx % n;
+      A[(m + i) * n + j] = make_double2(i == j ? s : 0.0, 0.0);
+    }
+  }
+  for (int idx = lane; idx < n * n; idx += 32) Rp[idx] = make_double2(0.0, 0.0);
+  __syncwarp();
+
+  const bool own = lane < n;
+  double norm = 0.0;
+  if (own)
+    for (int r = 0; r < ma; ++r) {
+      double2 a = A[r * n + lane];
+      norm = fma(a.x, a.x, fma(a.y, a.y, norm));
+    }
+  int logpos = lane;     // logical position of my physical column
+  bool chosen = !own;
+  int my_final = -1;     // final logical position (== step at which chosen)
+
+  for (int k = 0; k < n; ++k) {
+    // pivot: max downdated norm, ties -> smallest logical position (first max)
+    double bv = chosen ? -1.0 : norm;
+    int bp = chosen ? 0x7fffffff : logpos;
+    int bl = lane;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bl = ol; }
+    }
+    const int cp = bl;                      // physical pivot column
+    const int cp_pos = bp;                  // its current logical position
+    // exchange logical positions of column-at-k and the pivot column
+    if (!chosen && logpos == k) logpos = cp_pos;
+    if (lane == cp) { logpos = k; chosen = true; my_final = k; }
+
+    // r_kk from the pivot column (row-parallel reduction)
+    double part = 0.0;
+    for (int r = lane; r < ma; r += 32) {
+      double2 a = A[r * n + cp];
+      part = fma(a.x, a.x, fma(a.y, a.y, part));
+    }
+    double rkk = fmax(sqrt(warp_sum_d(part)), 1e-300);
+    __syncwarp();
+    for (int r = lane; r < ma; r += 32) {
+      double2 a = A[r * n + cp];
+      A[r * n + cp] = make_double2(a.x / rkk, a.y / rkk);
+    }
+    if (lane == 0) Rp[k * n + cp] = make_double2(rkk, 0.0);
+    __syncwarp();
+    if (!chosen) {
+      // proj = q^H a_j ; a_j -= q proj ; norm -= |proj|^2
+      double pr = 0.0, pi = 0.0;
+      for (int r = 0; r < ma; ++r) {
+        double2 q = A[r * n + cp];
+        double2 a = A[r * n + lane];
+        pr = fma(q.x, a.x, fma(q.y, a.y, pr));      // conj(q) * a
+        pi = fma(q.x, a.y, fma(-q.y, a.x, pi));
+      }
+      Rp[k * n + lane] = make_double2(pr, pi);
+      for (int r = 0; r < ma; ++r) {
+        double2 q = A[r * n + cp];
+        double2 a = A[r * n + lane];
+        a.x -= q.x * pr - q.y * pi;
+        a.y -= q.x * pi + q.y * pr;
+        A[r * n + lane] = a;
+      }
+      norm = fmax(norm - (pr * pr + pi * pi), 0.0);
+    }
+    __syncwarp();
+  }
+
+  // ---- outputs in logical order ----
+  // phys_of[logical] via shuffles: lane j (physical) knows my_final.
+  __shared__ int phys_of[MPNL_MAX_N];
+  if (own) phys_of[my_final] = lane;
+  __syncwarp();
+  int32_t* pc = perm_out + c * n;
+  double2* rc = r_out + c * (int64_t)n * n;
+  double2* qc = qh_out + c * (int64_t)n * m;
+  for (int idx = lane; idx < n; idx += 32) pc[idx] = phys_of[idx];
+  for (int idx = lane; idx < n * n; idx += 32) {
+    int i = idx / n, j = idx % n;
+    rc[idx] = (j >= i) ? Rp[i * n + phys_of[j]] : make_double2(0.0, 0.0);
+  }
+  for (int idx = lane; idx < n * m; idx += 32) {
+    int k = idx / m, r = idx % m;
+    double2 q = A[r * n + phys_of[k]];
+    qc[idx] = make_double2(q.x, -q.y);
+  }
+
+  // ---- fp32 traversal tables (see TableLayout) ----
+  if (tables == nullptr) return;
+  __syncwarp();
+  TableLayout tl(m, n);
+  float* tc = tables + c * (int64_t)tl.total;
+  const double nrm = qam_norm_d(L);
+  const double sc = 2.0 / nrm;
+  const double lv = (double)(L - 1) / nrm;
+  for (int idx = lane; idx < n * m; idx += 32) {
+    int k = idx / m, r = idx % m;
+    double2 q = A[r * n + phys_of[k]];
+    tc[tl.off_qh + 2 * idx] = (float)q.x;
+    tc[tl.off_qh + 2 * idx + 1] = (float)(-q.y);
+  }
+  for (int idx = lane; idx < n * tl.np_; idx += 32) {
+    int pos = idx / tl.np_, k = idx % tl.np_;   // column pos, row k
+    float2 v = make_float2(0.f, 0.f);
+    if (k < pos) {
+      double2 r = Rp[k * n + phys_of[pos]];
+      v = make_float2((float)(sc * r.x), (float)(sc * r.y));
+    }
+    tc[tl.off_rcol + 2 * idx] = v.x;
+    tc[tl.off_rcol + 2 * idx + 1] = v.y;
+  }
+  for (int k = lane; k < n; k += 32) {
+    double sr = 0.0, si = 0.0, ga = 0.0;
+    for (int j = k; j < n; ++j) {
+      double2 r = Rp[k * n + phys_of[j]];
+      sr += r.x;
+      si += r.y;
+      if (j > k) ga += sc * sqrt(r.x * r.x + r.y * r.y);
+    }
+    // shift = (L-1)(1+i)/norm * sum_{j>=k} r_kj
+    double shr = lv * (sr - si), shi = lv * (sr + si);
+    tc[tl.off_shift + 2 * k] = (float)shr;
+    tc[tl.off_shift + 2 * k + 1] = (float)shi;
+    double rkk = Rp[k * n + phys_of[k]].x;
+    double c2r = sc * rkk;
+    float* ly = tc + tl.off_lay + 4 * k;
+    ly[0] = (float)(-1.0 / (c2r * (L - 1)));
+    ly[1] = (float)c2r;
+    ly[2] = (float)(sqrt(shr * shr + shi * shi) + (L - 1) * 1.4142135623730951 * ga);
+    ly[3] = 0.f;
+  }
+}
+
+template __global__ void plan_qr_kernel<float2>(const float2*, int64_t, int, int, int, double,
+                                                int, int32_t*, double2*, double2*, float*);
+template __global__ void plan_qr_kernel<double2>(const double2*, int64_t, int, int, int, double,
+                                                 int, int32_t*, double2*, double2*, float*);
+
+cudaError_t launch_plan(const void* h, int h_is_f64, int64_t n_ch, int m, int n, int L,
+                        double noise_var, int augmented, int32_t* perm, double2* r64,
+                        double2* qh64, float* tables, cudaStream_t st) {
+  const int ma = augmented ? m + n : m;
+  size_t smem = (size_t)(ma * n + n * n) * sizeof(double2);
+  if (n_ch == 0) return cudaSuccess;
+  if (h_is_f64) {
+    cudaFuncSetAttribute(plan_qr_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    plan_qr_kernel<double2><<<(unsigned)n_ch, 32, smem, st>>>(
+        (const double2*)h, n_ch, m, n, L, noise_var, augmented, perm, r64, qh64, tables);
+  } else {
+    cudaFuncSetAttribute(plan_qr_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    plan_qr_kernel<float2><<<(unsigned)n_ch, 32, smem, st>>>(
+        (const float2*)h, n_ch, m, n, L, noise_var, augmented, perm, r64, qh64, tables);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace mpnl

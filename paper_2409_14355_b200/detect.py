@@ -1,0 +1,393 @@
+"""Drop-in MPNL detector API on the B200 kernels.
+
+Mirrors the MPNL part of the reference module `mpnlsim.detect`
+(`/root/reference/pkg/src/mpnlsim/detect.py`): same names, argument order,
+return types and error behaviour, backed by the C ABI of
+`include/mpnl_b200.h` (ctypes) — there is no CPU fallback.
+
+=========================  ==========================================  =====================
+this module                reference                                   kernels
+=========================  ==========================================  =====================
+allocate_expansions        detect.py:221-280                           host C++ port
+mpnl_plan_batch            detect.py:361-388 (+ _sorted_qr_batch)      K1 plan (fp64 QR)
+mpnl_detect_batch          detect.py:473-488 (full candidate list)     K5 exact (fp64)
+mpnl_detect_hard           hard composition cli.py:236-239,            K3 fp32 traversal +
+                           test_acceptance.py:114-117                  K5 fix-up of flags
+mpnl_preprocess            detect.py:391-400                           K1
+mpnl_detect                detect.py:491-506                           K5
+detect("mpnl", ...)        detect.py:563-576                           K1 + K5
+=========================  ==========================================  =====================
+
+Inputs may be numpy arrays (results come back as numpy, int64 labels /
+float64 metrics, like the reference) or CUDA torch tensors (results stay on
+the device: uint8 labels, float32/float64 metrics).  Extension over the
+reference: `y` may be (B, V, M) against a plan of B channels (V vectors per
+channel, e.g. the 168 REs of a resource block), equal to tiling the plan.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import warnings
+from dataclasses import dataclass, field
+from functools import cached_property
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import LLR_CLIP, Constellation, bits_from_labels
+
+__all__ = [
+    "allocate_expansions", "BatchPathPlan", "PathPlan", "mpnl_plan_batch",
+    "mpnl_preprocess", "mpnl_detect_batch", "mpnl_detect_hard", "mpnl_detect",
+    "detect", "DetectorInput", "CandidateList", "DetectionOutput",
+    "llr_from_candidates", "DETECTOR_NAMES", "SingularChannelError",
+]
+
+
+class SingularChannelError(ValueError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise _lib.MpnlError("MPNL kernels need a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _to_dev_complex(a, name):
+    """-> (contiguous CUDA complex tensor, is_f64, was_numpy)."""
+    if isinstance(a, torch.Tensor):
+        t = a
+        if not t.is_cuda:
+            t = t.to(_device())
+        if t.dtype not in (torch.complex64, torch.complex128):
+            t = t.to(torch.complex128)
+        return t.contiguous(), t.dtype == torch.complex128, False
+    arr = np.asarray(a)
+    if arr.dtype != np.complex64:
+        arr = arr.astype(np.complex128)
+    t = torch.from_numpy(np.ascontiguousarray(arr)).to(_device())
+    return t, arr.dtype == np.complex128, True
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+# ---------------------------------------------------------------------------
+# planning
+# ---------------------------------------------------------------------------
+
+def allocate_expansions(n_layers: int, q: int, n_paths: int,
+                        n_forced: int = 0) -> tuple[np.ndarray, int]:
+    """Per-layer expansion counts (tree position order) and realized paths.
+
+    Same rule and errors as detect.py:221-280 (computed by the C++ port)."""
+    lib = _lib.load()
+    out = np.zeros(max(int(n_layers), 1), dtype=np.int64)
+    realized = np.zeros(1, dtype=np.int64)
+    warned = np.zeros(1, dtype=np.int32)
+    rc = lib.mpnl_alloc_expansions(int(n_layers), int(q), int(n_paths), int(n_forced),
+                                   out.ctypes.data, realized.ctypes.data, warned.ctypes.data)
+    if warned[0]:
+        capped = min(int(n_paths), q ** n_layers)
+        warnings.warn(f"n_paths={capped} < {q}^{n_forced}: cannot fully expand all "
+                      "rank-deficient layers", UserWarning, stacklevel=2)
+    _lib.check(rc, "allocate_expansions")
+    return out[:n_layers], int(realized[0])
+
+
+@dataclass(frozen=True)
+class BatchPathPlan:
+    """Candidate-tree plans for a stack of channels (device resident).
+
+    Fields of the reference's BatchPathPlan (detect.py:283-302) are exposed
+    as numpy properties (`perm`, `qh`, `r`), materialised on first access."""
+
+    perm_dev: torch.Tensor = field(repr=False)     # (B, N) int32
+    r_dev: torch.Tensor = field(repr=False)        # (B, N, N) complex128
+    qh_dev: torch.Tensor = field(repr=False)       # (B, N, M) complex128
+    tables: torch.Tensor = field(repr=False)       # (B, T) float32, fast-path tables
+    expansions: np.ndarray = field(repr=False)     # (N,) int64
+    n_paths: int = 0
+    augmented: bool = False
+    noise_var: float = 0.0
+    order: int = 0
+    h_dev: torch.Tensor = field(default=None, repr=False)
+
+    @property
+    def batch(self) -> int:
+        return self.perm_dev.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.perm_dev.shape[1]
+
+    @property
+    def m(self) -> int:
+        return self.qh_dev.shape[2]
+
+    @cached_property
+    def perm(self) -> np.ndarray:
+        return self.perm_dev.cpu().numpy().astype(np.int64)
+
+    @cached_property
+    def qh(self) -> np.ndarray:
+        return self.qh_dev.cpu().numpy()
+
+    @cached_property
+    def r(self) -> np.ndarray:
+        return self.r_dev.cpu().numpy()
+
+    @cached_property
+    def fingerprint(self) -> bytes:
+        h = self.h_dev.cpu().numpy().astype(np.complex128)
+        return hashlib.sha1(h.tobytes()).digest()
+
+
+@dataclass(frozen=True)
+class PathPlan:
+    """Single-channel view (detect.py:305-318)."""
+
+    ordering: np.ndarray
+    q_factor: np.ndarray = field(repr=False)
+    r_factor: np.ndarray = field(repr=False)
+    expansions: np.ndarray
+    n_paths: int
+    requested_paths: int
+    channel: np.ndarray = field(repr=False)
+    noise_var: float = 0.0
+    fingerprint: bytes = b""
+    _batch: BatchPathPlan = field(default=None, repr=False)
+
+
+def mpnl_plan_batch(h, noise_var: float, n_paths: int, c: Constellation) -> BatchPathPlan:
+    """Plan candidate trees for a (B, M, N) channel stack (detect.py:361-388).
+
+    Sorted QR in fp64 on the GPU (K1).  Overloaded channels (N > M) are
+    planned on [H; sqrt(nv) I] with the top N - M layers forced full."""
+    lib = _lib.load()
+    hd, h64, _ = _to_dev_complex(h, "h")
+    if hd.dim() == 2:
+        hd = hd.unsqueeze(0)
+    b, m, n = hd.shape
+    expansions, realized = allocate_expansions(n, c.order, n_paths, n_forced=max(0, n - m))
+    dev = hd.device
+    perm = torch.empty((b, n), dtype=torch.int32, device=dev)
+    r = torch.empty((b, n, n), dtype=torch.complex128, device=dev)
+    qh = torch.empty((b, n, m), dtype=torch.complex128, device=dev)
+    tables = torch.empty((b, int(lib.mpnl_tables_floats(m, n))), dtype=torch.float32, device=dev)
+    rc = lib.mpnl_plan(hd.data_ptr(), int(h64), b, m, n, c.order, float(noise_var),
+                       perm.data_ptr(), r.data_ptr(), qh.data_ptr(), tables.data_ptr(), _stream())
+    _lib.check(rc, "mpnl_plan")
+    return BatchPathPlan(perm_dev=perm, r_dev=r, qh_dev=qh, tables=tables,
+                         expansions=expansions, n_paths=realized, augmented=n > m,
+                         noise_var=float(noise_var), order=c.order, h_dev=hd)
+
+
+def mpnl_preprocess(h, noise_var: float, n_paths: int, c: Constellation) -> PathPlan:
+    """Channel-time planning for a single matrix (detect.py:391-400)."""
+    h = np.asarray(h, dtype=complex)
+    bp = mpnl_plan_batch(h[None], noise_var, n_paths, c)
+    return PathPlan(ordering=bp.perm[0], q_factor=bp.qh[0].conj().T, r_factor=bp.r[0],
+                    expansions=bp.expansions, n_paths=bp.n_paths, requested_paths=n_paths,
+                    channel=h, noise_var=noise_var,
+                    fingerprint=hashlib.sha1(h.tobytes()).digest(), _batch=bp)
+
+
+# ---------------------------------------------------------------------------
+# detection
+# ---------------------------------------------------------------------------
+
+def _shape_y(plan: BatchPathPlan, y):
+    yd, y64, was_np = _to_dev_complex(y, "y")
+    if yd.dim() == 1:
+        yd = yd.reshape(1, 1, -1)
+        squeeze = "vec"
+    elif yd.dim() == 2:
+        yd = yd.reshape(yd.shape[0], 1, yd.shape[1])
+        squeeze = "batch"
+    else:
+        squeeze = None
+    if yd.shape[0] != plan.batch or yd.shape[2] != plan.m:
+        raise ValueError("inconsistent channel/observation dimensions")
+    return yd.contiguous(), y64, was_np, squeeze
+
+
+def mpnl_detect_hard(plan: BatchPathPlan, h, y, c: Constellation, *, return_flags=False):
+    """Hard-output MPNL: (hard labels (..., N), min_metric (...)).
+
+    Equals `take_along_axis(labels, best)` / `metrics[best]` of
+    `mpnl_detect_batch` (cli.py:236-239).  fp32 traversal kernel with an
+    in-kernel guard; guarded vectors are recomputed in fp64 on the GPU.
+    `h` is accepted for signature parity (the metric uses the plan)."""
+    lib = _lib.load()
+    if c.order != plan.order:
+        raise ValueError("constellation does not match the plan")
+    yd, y64, was_np, squeeze = _shape_y(plan, y)
+    nch, v, m = yd.shape
+    n = plan.n
+    dev = yd.device
+    hard = torch.empty((nch, v, n), dtype=torch.uint8, device=dev)
+    metric = torch.empty((nch, v), dtype=torch.float32, device=dev)
+    flags = torch.empty((nch, v), dtype=torch.uint8, device=dev) if return_flags else None
+    ws = torch.empty(int(lib.mpnl_workspace_bytes(nch * v)), dtype=torch.uint8, device=dev)
+    rc = lib.mpnl_detect_hard(plan.perm_dev.data_ptr(), plan.r_dev.data_ptr(),
+                              plan.qh_dev.data_ptr(), plan.tables.data_ptr(), yd.data_ptr(),
+                              int(y64), nch, v, m, n, c.order, plan.expansions.ctypes.data,
+                              plan.noise_var, hard.data_ptr(), metric.data_ptr(), _ptr(flags),
+                              ws.data_ptr(), ws.numel(), _stream())
+    _lib.check(rc, "mpnl_detect_hard")
+    outs = [hard, metric] + ([flags] if return_flags else [])
+    if squeeze == "batch":
+        outs = [o[:, 0] for o in outs]
+    elif squeeze == "vec":
+        outs = [o[0, 0] for o in outs]
+    if was_np:
+        outs = [outs[0].cpu().numpy().astype(np.int64), outs[1].cpu().numpy().astype(np.float64)
+                ] + ([outs[2].cpu().numpy().astype(bool)] if return_flags else [])
+    return tuple(outs)
+
+
+def mpnl_detect_batch(plan: BatchPathPlan, h, y, c: Constellation):
+    """Full parallel-path search (detect.py:473-488).
+
+    Returns (labels (B, P, N), metrics (B, P), best (B,)): labels in path
+    order (mixed radix, top layer most significant) and stream order,
+    metrics = ||y - Hx||^2, best by (metric, labels) total order.  fp64
+    kernel with the reference's decision rules."""
+    lib = _lib.load()
+    if c.order != plan.order:
+        raise ValueError("constellation does not match the plan")
+    yd, y64, was_np, squeeze = _shape_y(plan, y)
+    nch, v, m = yd.shape
+    n, p = plan.n, plan.n_paths
+    dev = yd.device
+    labels = torch.empty((nch, v, p, n), dtype=torch.uint8, device=dev)
+    metrics = torch.empty((nch, v, p), dtype=torch.float64, device=dev)
+    best = torch.empty((nch, v), dtype=torch.int64, device=dev)
+    rc = lib.mpnl_detect_full(plan.perm_dev.data_ptr(), plan.r_dev.data_ptr(),
+                              plan.qh_dev.data_ptr(), yd.data_ptr(), int(y64), nch, v, m, n,
+                              c.order, plan.expansions.ctypes.data, plan.noise_var,
+                              labels.data_ptr(), metrics.data_ptr(), best.data_ptr(), _stream())
+    _lib.check(rc, "mpnl_detect_batch")
+    outs = [labels, metrics, best]
+    if squeeze == "batch":
+        outs = [o[:, 0] for o in outs]
+    elif squeeze == "vec":
+        outs = [o[0, 0] for o in outs]
+    if was_np:
+        outs = [outs[0].cpu().numpy().astype(np.int64), outs[1].cpu().numpy(),
+                outs[2].cpu().numpy()]
+    return tuple(outs)
+
+
+# ---------------------------------------------------------------------------
+# single-instance API (detect.py:30-77, 456-506, 560-576)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class DetectorInput:
+    h: np.ndarray
+    y: np.ndarray
+    noise_var: float
+    constellation: Constellation
+
+    def __post_init__(self):
+        h = np.asarray(self.h, dtype=complex)
+        y = np.asarray(self.y, dtype=complex).ravel()
+        if h.ndim != 2 or y.size != h.shape[0]:
+            raise ValueError("inconsistent channel/observation dimensions")
+        if self.noise_var <= 0:
+            raise ValueError("noise_var must be positive")
+        object.__setattr__(self, "h", h)
+        object.__setattr__(self, "y", y)
+
+    @property
+    def m(self) -> int:
+        return self.h.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.h.shape[1]
+
+
+@dataclass(frozen=True)
+class CandidateList:
+    candidates: np.ndarray = field(repr=False)
+    labels: np.ndarray = field(repr=False)
+    metrics: np.ndarray = field(repr=False)
+
+    @property
+    def n_paths(self) -> int:
+        return self.candidates.shape[0]
+
+
+@dataclass(frozen=True)
+class DetectionOutput:
+    hard: np.ndarray = field(repr=False)
+    hard_labels: np.ndarray = field(repr=False)
+    llrs: np.ndarray = field(repr=False)
+    min_metric: float
+    soft: np.ndarray | None = field(default=None, repr=False)
+
+
+def _residual_metric(h, y, x):
+    r = y - h @ x
+    return float(np.real(np.vdot(r, r)))
+
+
+def llr_from_candidates(clist: CandidateList, noise_var: float, c: Constellation,
+                        clip: float = LLR_CLIP) -> np.ndarray:
+    """List max-log LLRs over a candidate list (detect.py:440-462); host-side
+    post-processing of one GPU candidate list for the single-instance API."""
+    if clist.n_paths < 1:
+        raise ValueError("empty candidate list")
+    bits = bits_from_labels(clist.labels, c).astype(bool)   # (P, N, bps)
+    mm = clist.metrics[:, None, None]
+    min1 = np.where(bits, mm, np.inf).min(axis=0)
+    min0 = np.where(~bits, mm, np.inf).min(axis=0)
+    with np.errstate(invalid="ignore"):
+        llr = (min1 - min0) / noise_var
+    return np.clip(llr, -clip, clip)
+
+
+def mpnl_detect(plan: PathPlan, inp: DetectorInput):
+    """Evaluate the planned candidate paths for one observation."""
+    fp = hashlib.sha1(np.asarray(inp.h, dtype=complex).tobytes()).digest()
+    if fp != plan.fingerprint:
+        raise ValueError("plan/channel fingerprint mismatch")
+    c = inp.constellation
+    labels, metrics, best = mpnl_detect_batch(plan._batch, inp.h[None], inp.y[None], c)
+    labels, metrics, b = labels[0], metrics[0], int(best[0])
+    cands = c.points[labels]
+    clist = CandidateList(candidates=cands, labels=labels, metrics=metrics)
+    llrs = llr_from_candidates(clist, inp.noise_var, c)
+    hard = cands[b]
+    out = DetectionOutput(hard=hard, hard_labels=labels[b], llrs=llrs,
+                          min_metric=_residual_metric(inp.h, inp.y, hard))
+    return clist, out
+
+
+DETECTOR_NAMES = ("mpnl",)
+
+
+def detect(name: str, inp: DetectorInput, n_paths: int = 32) -> DetectionOutput:
+    """Name dispatch (detect.py:563-576).  Only the MPNL path is in scope for
+    this library; the reference's zf/mmse/ml/sphere stay in the reference."""
+    if name == "mpnl":
+        plan = mpnl_preprocess(inp.h, inp.noise_var, n_paths, inp.constellation)
+        return mpnl_detect(plan, inp)[1]
+    if name in ("zf", "mmse", "ml", "sphere"):
+        raise NotImplementedError(f"detector {name!r} is outside the MPNL hot path")
+    raise ValueError(f"unknown detector {name!r}")

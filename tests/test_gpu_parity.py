@@ -1,0 +1,162 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden outputs (tests/golden, made by importing the reference) and against
+the CPU oracle on fresh seeded inputs.
+
+Bar (BASELINE.json north star):
+* hard labels identical except where the oracle's two lowest path metrics
+  tie within 1e-5 relative;
+* winning metric within 1e-4 relative (fp32 fast path);
+* full candidate list (fp64 kernel): labels/best identical, metrics 1e-9.
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import mpnl_oracle as orc
+from paper_2409_14355_b200.core import constellation_for
+from paper_2409_14355_b200.workloads import CONFIGS, generate
+
+GOLD = Path(__file__).resolve().parent / "golden"
+pytestmark = pytest.mark.gpu
+
+TIE_REL = 1e-5
+METRIC_REL = 1e-4
+
+
+def _det():
+    from paper_2409_14355_b200 import detect
+    return detect
+
+
+def _check_hard(hard, metric, ref_hard, m1, m2, what):
+    hard = np.asarray(hard).reshape(ref_hard.shape)
+    metric = np.asarray(metric).reshape(m1.shape)
+    exempt = (m2 - m1) <= TIE_REL * m1
+    bad = np.any(hard != ref_hard, axis=-1) & ~exempt
+    assert not bad.any(), f"{what}: {int(bad.sum())} vectors differ (of {bad.size}), " \
+                          f"first at {np.argwhere(bad)[:3].tolist()}"
+    rel = np.abs(metric - m1) / np.maximum(m1, 1e-30)
+    assert np.all(rel[~exempt] <= METRIC_REL), f"{what}: metric rel err {rel.max():.2e}"
+    return int(exempt.sum())
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4", "C5P64"])
+def test_plan_matches_reference(name):
+    det = _det()
+    g = np.load(GOLD / "plan.npz")
+    h = g[f"{name}_h"]
+    cfg = CONFIGS[name]
+    plan = det.mpnl_plan_batch(h, 0.1, cfg.n_paths, constellation_for(cfg.order))
+    assert np.array_equal(plan.perm, g[f"{name}_perm"])
+    assert np.array_equal(plan.expansions, g[f"{name}_exp"])
+    np.testing.assert_allclose(plan.r, g[f"{name}_r"], rtol=0, atol=1e-11)
+    np.testing.assert_allclose(plan.qh, g[f"{name}_qh"], rtol=0, atol=1e-11)
+
+
+def test_plan_overloaded_matches_reference():
+    det = _det()
+    g = np.load(GOLD / "plan.npz")
+    plan = det.mpnl_plan_batch(g["over_h"], 0.1, 32, constellation_for(4))
+    assert plan.augmented
+    assert np.array_equal(plan.perm, g["over_perm"])
+    assert np.array_equal(plan.expansions, g["over_exp"])
+    np.testing.assert_allclose(plan.r, g["over_r"], atol=1e-11)
+    np.testing.assert_allclose(plan.qh, g["over_qh"], atol=1e-11)
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_hard_matches_reference_golden(name):
+    det = _det()
+    g = np.load(GOLD / f"hard_{name}.npz")
+    c = constellation_for(int(g["order"]))
+    plan = det.mpnl_plan_batch(g["h"], float(g["nv"]), int(g["n_paths"]), c)
+    hard, metric, flags = det.mpnl_detect_hard(plan, g["h"], g["y"], c, return_flags=True)
+    _check_hard(hard, metric, g["hard"], g["m1"], g["m2"], name)
+    print(f"{name}: flagged {flags.mean():.4%}")
+
+
+@pytest.mark.parametrize("tag", ["c1", "c2", "c5p16", "c5p256"])
+def test_full_list_matches_reference_golden(tag):
+    det = _det()
+    g = np.load(GOLD / f"full_{tag}.npz")
+    c = constellation_for(int(g["order"]))
+    plan = det.mpnl_plan_batch(g["h"], float(g["nv"]), int(g["n_paths"]), c)
+    lab, met, best = det.mpnl_detect_batch(plan, g["h"], g["y"], c)
+    lab, met, best = lab[0], met[0], best[0]
+    assert np.array_equal(lab, g["labels"]), "path-ordered labels differ"
+    np.testing.assert_allclose(met, g["metrics"], rtol=1e-9)
+    assert np.array_equal(best, g["best"])
+
+
+@pytest.mark.parametrize("tag", ["q4x4", "q4full", "over2x3", "q16_4x4"])
+def test_full_list_small_cases(tag):
+    det = _det()
+    g = np.load(GOLD / f"full_{tag}.npz")
+    c = constellation_for(int(g["order"]))
+    plan = det.mpnl_plan_batch(g["h"], float(g["nv"]), int(g["n_paths"]), c)
+    assert np.array_equal(plan.perm, g["perm"])
+    lab, met, best = det.mpnl_detect_batch(plan, g["h"], g["y"], c)
+    assert np.array_equal(lab, g["labels"])
+    np.testing.assert_allclose(met, g["metrics"], rtol=1e-9, atol=1e-12)
+    assert np.array_equal(best, g["best"])
+    hard, m1 = det.mpnl_detect_hard(plan, g["h"], g["y"], c)
+    rows = np.arange(len(best))
+    assert np.array_equal(hard, g["labels"][rows, g["best"]])
+    np.testing.assert_allclose(m1, g["metrics"][rows, g["best"]], rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("name,n_rb", [("C1", 4), ("C2", 6), ("C3", 6), ("C4", 3),
+                                       ("C5P16", 12), ("C5P64", 6), ("C5P256", 3)])
+def test_hard_vs_oracle_fresh_inputs(name, n_rb):
+    """Fresh seeded RBs (not in the golden set) against the CPU oracle."""
+    det = _det()
+    d = generate(name, seed=99, n_rb=n_rb, rb_offset=1000)
+    cfg = d["cfg"]
+    c = constellation_for(cfg.order)
+    ref_hard, m1, m2 = orc.detect_rb_parallel(d["h"], d["y"], d["nv"][0], cfg.n_paths,
+                                              cfg.order, rbs_per_task=1)
+    plan = det.mpnl_plan_batch(d["h"], d["nv"][0], cfg.n_paths, c)
+    hard, metric = det.mpnl_detect_hard(plan, d["h"], d["y"], c)
+    _check_hard(hard, metric, ref_hard.astype(np.uint8), m1, m2, name)
+
+
+def test_deterministic_across_chunking():
+    """Bit-identical outputs regardless of how vectors are grouped into calls."""
+    import torch
+    det = _det()
+    d = generate("C2", n_rb=3)
+    c = constellation_for(16)
+    h = torch.from_numpy(d["h"]).cuda()
+    y = torch.from_numpy(d["y"]).cuda()
+    plan = det.mpnl_plan_batch(h, 0.5, 64, c)
+    a_h, a_m = det.mpnl_detect_hard(plan, h, y, c)
+    b_h, b_m = det.mpnl_detect_hard(plan, h, y, c)
+    assert torch.equal(a_h, b_h) and torch.equal(a_m, b_m)
+    # per-channel calls with half the vectors each
+    for ch in range(3):
+        sub = det.mpnl_plan_batch(h[ch:ch + 1], 0.5, 64, c)
+        for lo, hi in ((0, 500), (500, 1008)):
+            s_h, s_m = det.mpnl_detect_hard(sub, h[ch:ch + 1], y[ch:ch + 1, lo:hi].contiguous(), c)
+            assert torch.equal(s_h[0], a_h[ch, lo:hi])
+            assert torch.equal(s_m[0], a_m[ch, lo:hi])
+
+
+@pytest.mark.parametrize("name", ["C2", "C5P1024"])
+def test_noiseless_round_trip_full_size(name):
+    """Size-independent property at full config size: y = Hx exactly ->
+    every vector decodes to x (reference test_detect.py:290-299 at scale)."""
+    import torch
+    det = _det()
+    cfg = CONFIGS[name]
+    n_rb = cfg.n_rb if name == "C2" else 256
+    d = generate(name, seed=5, n_rb=n_rb)
+    c = constellation_for(cfg.order)
+    h = torch.from_numpy(d["h"]).cuda()
+    x = torch.from_numpy(c.points[d["labels"]]).cuda()
+    y = torch.einsum("cmn,cvn->cvm", h.to(torch.complex128), x).to(torch.complex64)
+    plan = det.mpnl_plan_batch(h, 0.01, cfg.n_paths, c)
+    hard, metric = det.mpnl_detect_hard(plan, h, y, c)
+    assert torch.equal(hard.long().cpu(), torch.from_numpy(d["labels"]))
+    assert float(metric.max()) < 1e-4
