@@ -176,9 +176,16 @@ exact_kernel(const ExactArgs a, const TreeParams tp) {
     }
     if (lane == 0) {
       const uint8_t* wl = wsm + so.blab + bl * 32;
-      if (a.hard)
+      // Fix-up mode: when the fp64 winner equals the fp32 winner, keep the
+      // fp32 result untouched, so outputs never depend on which vectors a
+      // chunk-dependent guard happened to flag (the labels cannot: the guard
+      // bound is valid for every chunking).
+      bool same = a.list != nullptr && a.hard != nullptr;
+      if (same)
+        for (int k = 0; k < n; ++k) same = same && a.hard[gv * n + k] == wl[k];
+      if (a.hard && !same)
         for (int k = 0; k < n; ++k) a.hard[gv * n + k] = wl[k];
-      if (a.metric) a.metric[gv] = (float)bm;
+      if (a.metric && !same) a.metric[gv] = (float)bm;
       if (a.metric64) a.metric64[gv] = bm;
       if (a.full_best) a.full_best[gv] = bp;
     }
