@@ -175,8 +175,9 @@ def run_gpu(args, rank, world):
     realized = plan.n_paths
     hard = torch.empty((y.shape[0], y.shape[1], cfg.n), dtype=torch.uint8, device=dev)
     metric = torch.empty((y.shape[0], y.shape[1]), dtype=torch.float32, device=dev)
-    ws = torch.empty(int(lib.mpnl_workspace_bytes(nvec)), dtype=torch.uint8, device=dev)
     ex = plan.expansions
+    ws = torch.empty(int(lib.mpnl_workspace_bytes(nvec, cfg.n, cfg.order, ex.ctypes.data)),
+                     dtype=torch.uint8, device=dev)
 
     def step(ev_k0=None, ev_k1=None):
         p = det.mpnl_plan_batch(h, nv, cfg.n_paths, c)
@@ -184,12 +185,14 @@ def run_gpu(args, rank, world):
                  p.tables.data_ptr(), y.data_ptr(), 0, y.shape[0], y.shape[1], cfg.m, cfg.n,
                  cfg.order, ex.ctypes.data, nv, hard.data_ptr(), metric.data_ptr(), None,
                  ws.data_ptr(), ws.numel(), stream.cuda_stream)
+        _lib.check(lib.mpnl_detect_hard_stage(1, *args_), "stage1")
         if ev_k0 is not None:
             ev_k0.record(stream)
-        _lib.check(lib.mpnl_detect_hard_stage(1, *args_), "stage1")
+        _lib.check(lib.mpnl_detect_hard_stage(2, *args_), "stage2")   # traversal kernel
         if ev_k1 is not None:
             ev_k1.record(stream)
-        _lib.check(lib.mpnl_detect_hard_stage(2, *args_), "stage2")
+        _lib.check(lib.mpnl_detect_hard_stage(3, *args_), "stage3")
+        _lib.check(lib.mpnl_detect_hard_stage(4, *args_), "stage4")
 
     for _ in range(args.warmup):
         step()

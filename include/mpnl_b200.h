@@ -56,8 +56,10 @@ int mpnl_plan(const void* h, int h_is_f64, int64_t n_ch, int m, int n, int q,
               double noise_var, int32_t* perm, void* r64, void* qh64,
               float* tables, void* stream);
 
-/* Scratch bytes mpnl_detect_hard needs for n_vectors received vectors. */
-int64_t mpnl_workspace_bytes(int64_t n_vectors);
+/* Scratch bytes mpnl_detect_hard needs for n_vectors received vectors of a
+ * plan with these expansions (-1 on invalid arguments). */
+int64_t mpnl_workspace_bytes(int64_t n_vectors, int n, int q,
+                             const int64_t* expansions);
 
 /* Hard-output detection of y (n_ch, v_per_ch, m) (complex64 or complex128)
  * against the plan: writes hard (n_ch*v_per_ch, n) uint8 point labels in
@@ -72,8 +74,10 @@ int mpnl_detect_hard(const int32_t* perm, const void* r64, const void* qh64,
                      uint8_t* hard, float* metric, uint8_t* flags,
                      void* workspace, int64_t workspace_bytes, void* stream);
 
-/* The two stages of mpnl_detect_hard, for timing: stage 1 = fp32 traversal
- * (+ flag list), stage 2 = fp64 fix-up of the flagged vectors. */
+/* The stages of mpnl_detect_hard, for timing (all four, in order, equal
+ * mpnl_detect_hard): 1 = reset + partial-layer selection kernel, 2 = fp32
+ * traversal kernel (the hot kernel), 3 = verification kernel (winner labels,
+ * fp64 re-decision of guarded decisions), 4 = fp64 fix-up kernel. */
 int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64,
                            const void* qh64, const float* tables, const void* y,
                            int y_is_f64, int64_t n_ch, int64_t v_per_ch, int m,
@@ -92,8 +96,14 @@ int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64,
                      uint8_t* labels, double* metrics, int64_t* best,
                      void* stream);
 
-/* Guard scale c in tau = c * 2^-24 (default 2(m+n)+16 when c <= 0). */
+/* Scale of the fp32 error bound used by the traversal guard (default 1 =
+ * the rigorous bound; <= 0 restores the default).  Diagnostics only. */
 void mpnl_set_guard_scale(double c);
+
+/* Optional device int32[4] counters: [0] += guard events logged, [1] +=
+ * events re-decided in fp64, [2] += near-ties resolved in fp64, [3] +=
+ * vectors sent to the fp64 kernel (NULL disables).  Diagnostics only. */
+void mpnl_set_stats(int32_t* device_counters);
 
 /* FFMA throughput probe (for the roofline denominator): runs `iters` dependent
  * FFMA chains on every SM; returns FLOPs executed.  out: device float[blocks*threads]. */

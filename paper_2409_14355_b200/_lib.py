@@ -24,7 +24,7 @@ _SIGS = {
     "mpnl_alloc_expansions": ([_i32, _i32, _i64, _i32, _vp, _vp, _vp], _i32),
     "mpnl_tables_floats": ([_i32, _i32], _i64),
     "mpnl_plan": ([_vp, _i32, _i64, _i32, _i32, _i32, _f64, _vp, _vp, _vp, _vp, _vp], _i32),
-    "mpnl_workspace_bytes": ([_i64], _i64),
+    "mpnl_workspace_bytes": ([_i64, _i32, _i32, _vp], _i64),
     "mpnl_detect_hard": ([_vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _vp,
                           _f64, _vp, _vp, _vp, _vp, _i64, _vp], _i32),
     "mpnl_detect_hard_stage": ([_i32, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32,
@@ -32,6 +32,7 @@ _SIGS = {
     "mpnl_detect_full": ([_vp, _vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _vp, _f64,
                           _vp, _vp, _vp, _vp], _i32),
     "mpnl_set_guard_scale": ([_f64], None),
+    "mpnl_set_stats": ([_vp], None),
     "mpnl_ffma_probe": ([_vp, _i32, _i32, _i32, _vp], _i64),
 }
 

@@ -19,10 +19,10 @@ namespace mpnl {
 cudaError_t launch_plan(const void* h, int h_is_f64, int64_t n_ch, int m, int n, int L,
                         double noise_var, int augmented, int32_t* perm, double2* r64,
                         double2* qh64, float* tables, cudaStream_t st);
-#define MPNL_DECL_PART(LL, PP)                                                             \
-  cudaError_t launch_traverse_l##LL##_p##PP(int n, const TraverseArgs& a, const TreeParams& tp, \
-                                            int threads, unsigned grid, size_t smem,       \
-                                            cudaStream_t st);
+#define MPNL_DECL_PART(LL, PP)                                                                 \
+  cudaError_t launch_fast_l##LL##_p##PP(int n, int kind, const DetectArgs& a, const TreeParams& tp, \
+                                        unsigned grid, int threads, size_t smem, int extra,       \
+                                        cudaStream_t st);
 MPNL_DECL_PART(2, 0) MPNL_DECL_PART(2, 1) MPNL_DECL_PART(2, 2) MPNL_DECL_PART(2, 3)
 MPNL_DECL_PART(4, 0) MPNL_DECL_PART(4, 1) MPNL_DECL_PART(4, 2) MPNL_DECL_PART(4, 3)
 MPNL_DECL_PART(8, 0) MPNL_DECL_PART(8, 1) MPNL_DECL_PART(8, 2) MPNL_DECL_PART(8, 3)
@@ -35,12 +35,24 @@ namespace mpnl {
 cudaError_t launch_exact(const ExactArgs& a, const TreeParams& tp, int grid, cudaStream_t st);
 }
 
+__global__ void flags_kernel(uint8_t* flags, const uint32_t* vflag, int64_t B, int all) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < B) flags[i] = (all || vflag[i]) ? 1 : 0;
+}
+
+static cudaError_t launch_flags(uint8_t* flags, const uint32_t* vflag, int64_t B, int all,
+                                cudaStream_t st) {
+  flags_kernel<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(flags, vflag, B, all);
+  return cudaGetLastError();
+}
+
 using namespace mpnl;
 
 namespace {
 
 thread_local std::string g_err;
 double g_guard_scale = 0.0;
+int32_t* g_stats = nullptr;
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -107,12 +119,11 @@ TreeBuild build_tree(int n, int L, const int64_t* ex) {
     if (e < q) {
       b.tp.list_off[pos] = off;
       off += b.tp.n_paths / b.tp.stride[pos];
-      int cnt = 0;
-      for (int i = 0; i < L; ++i)
-        for (int j = 0; j < L; ++j)
-          if ((i + 1) * (j + 1) <= e + 1) ++cnt;
-      b.tp.stair_cnt[pos] = cnt;
     }
+  }
+  for (int pos = 0; pos < n; ++pos) {
+    b.tp.ms[pos] = div_magic((unsigned)b.tp.stride[pos]);
+    b.tp.me[pos] = div_magic((unsigned)b.tp.e[pos]);
   }
   b.tp.list_bytes = off;
   b.ok = true;
@@ -128,13 +139,6 @@ int check_dims(int m, int n, int q) {
   return MPNL_OK;
 }
 
-struct Launch {
-  TraverseArgs a;
-  int threads;
-  unsigned grid;
-  size_t smem;
-};
-
 int trav_pt(int n) {
   switch ((n + 7) / 8) {
     case 1: return TravCfg<8>::PT;
@@ -143,16 +147,16 @@ int trav_pt(int n) {
     default: return TravCfg<32>::PT;
   }
 }
-int trav_maxt(int n) { return n <= 16 ? TravCfg<16>::MAXT : TravCfg<32>::MAXT; }
 
-cudaError_t launch_traverse(int n, int L, const Launch& l, const TreeParams& tp, cudaStream_t st) {
+cudaError_t launch_fast(int n, int L, int kind, const DetectArgs& a, const TreeParams& tp,
+                        unsigned grid, int threads, size_t smem, int extra, cudaStream_t st) {
   const int part = (n - 1) / 8;
-#define MPNL_PART(LL)                                                                    \
-  switch (part) {                                                                        \
-    case 0: return launch_traverse_l##LL##_p0(n, l.a, tp, l.threads, l.grid, l.smem, st); \
-    case 1: return launch_traverse_l##LL##_p1(n, l.a, tp, l.threads, l.grid, l.smem, st); \
-    case 2: return launch_traverse_l##LL##_p2(n, l.a, tp, l.threads, l.grid, l.smem, st); \
-    default: return launch_traverse_l##LL##_p3(n, l.a, tp, l.threads, l.grid, l.smem, st); \
+#define MPNL_PART(LL)                                                                       \
+  switch (part) {                                                                           \
+    case 0: return launch_fast_l##LL##_p0(n, kind, a, tp, grid, threads, smem, extra, st); \
+    case 1: return launch_fast_l##LL##_p1(n, kind, a, tp, grid, threads, smem, extra, st); \
+    case 2: return launch_fast_l##LL##_p2(n, kind, a, tp, grid, threads, smem, extra, st); \
+    default: return launch_fast_l##LL##_p3(n, kind, a, tp, grid, threads, smem, extra, st); \
   }
   if (L == 2) { MPNL_PART(2) }
   if (L == 4) { MPNL_PART(4) }
@@ -160,47 +164,26 @@ cudaError_t launch_traverse(int n, int L, const Launch& l, const TreeParams& tp,
 #undef MPNL_PART
 }
 
-// Work decomposition of one channel's V vectors into CTA chunks (see
-// traverse.cuh phase C): VPI mode packs S/P vectors per warp item when P
-// divides S = 32*PT, batch mode loops ceil(P/S) slot batches per vector.
-bool plan_launch(int n, int m, int L, int64_t n_ch, int64_t V, const TreeParams& tp, Launch& l,
-                 std::string& err) {
-  const int pt = trav_pt(n), S = 32 * pt, P = tp.n_paths;
-  int vpi = 1, bpv = 1;
-  if (P < S && S % P == 0) vpi = S / P;
-  else bpv = (P + S - 1) / S;
-  const int maxt = trav_maxt(n);
-  const int warps = maxt / 32;
-  const int64_t items_ch = (V + vpi - 1) / vpi;
-  // items per CTA: a multiple of the warp count, ~4096 path slots per warp pass
-  int64_t per_warp = std::max<int64_t>(1, 4096 / ((int64_t)S * bpv * warps));
-  int64_t ipc = std::min<int64_t>(items_ch, warps * per_warp);
-  int vc = (int)std::min<int64_t>(V, ipc * vpi);
-  const int ngroups = maxt / MPNL_GROUP;
-  while (vc > 1 && TravSmem(m, n, vc, tp.list_bytes, ngroups).total_bytes > 200 * 1024) vc = (vc + 1) / 2;
-  const TravSmem so(m, n, vc, tp.list_bytes, ngroups);
-  if (so.total_bytes > 220 * 1024) { err = "shared-memory plan exceeds 220 KB"; return false; }
-  const int64_t chunks = (V + vc - 1) / vc;
-  if (n_ch * chunks > 0x7fffffffLL) { err = "grid too large"; return false; }
-  std::memset(&l.a, 0, sizeof(l.a));
-  l.a.V = V;
-  l.a.n_ch = n_ch;
-  l.a.m = m;
-  l.a.vc = vc;
-  l.a.chunks = (int)chunks;
-  l.a.vpi = vpi;
-  l.a.bpv = bpv;
-  int has_partial = 0;
-  for (int pos = n - 1; pos >= n - tp.n_top; --pos) has_partial |= tp.e[pos] < L * L;
-  l.a.has_partial = has_partial;
-  l.a.metric_offset = m > n;
-  const double cg = g_guard_scale > 0 ? g_guard_scale : 2.0 * (m + n) + 16.0;
-  l.a.tau = (float)(cg * std::ldexp(1.0, -24));
-  l.threads = maxt;
-  l.grid = (unsigned)(n_ch * chunks);
-  l.smem = so.total_bytes;
-  return true;
-}
+// Workspace carve-up (byte offsets), identical in mpnl_workspace_bytes and the launches.
+struct Workspace {
+  int64_t counters, fix_list, vflag, vres, vpath, events, lists, zq, total;
+  int64_t ev_cap;
+  Workspace(int64_t B, int list_bytes, int n) {
+    auto up = [](int64_t x) { return (x + 255) & ~int64_t(255); };
+    B = std::max<int64_t>(B, 1);
+    ev_cap = std::min<int64_t>(8 * B + 4096, int64_t(1) << 30);
+    int64_t o = 0;
+    counters = o; o = up(o + 16);
+    fix_list = o; o = up(o + 8 * B);
+    vflag = o; o = up(o + 4 * B);
+    vres = o; o = up(o + 16 * B);
+    vpath = o; o = up(o + 8 * B);
+    events = o; o = up(o + 16 * ev_cap);
+    lists = o; o = up(o + B * (int64_t)list_bytes);
+    zq = o; o = up(o + B * 8 * (int64_t)n);
+    total = o;
+  }
+};
 
 }  // namespace
 
@@ -212,6 +195,8 @@ const char* mpnl_last_error(void) { return g_err.c_str(); }
 int mpnl_version(void) { return 0x000100; }
 
 void mpnl_set_guard_scale(double c) { g_guard_scale = c; }
+
+void mpnl_set_stats(int32_t* device_counters) { g_stats = device_counters; }
 
 int mpnl_alloc_expansions(int n_layers, int q, int64_t n_paths, int n_forced,
                           int64_t* expansions_out, int64_t* realized_out, int* warned) {
@@ -251,7 +236,13 @@ int mpnl_alloc_expansions(int n_layers, int q, int64_t n_paths, int n_forced,
 
 int64_t mpnl_tables_floats(int m, int n) { return TableLayout(m, n).total; }
 
-int64_t mpnl_workspace_bytes(int64_t n_vectors) { return 16 + 8 * std::max<int64_t>(n_vectors, 1); }
+int64_t mpnl_workspace_bytes(int64_t n_vectors, int n, int q, const int64_t* expansions) {
+  const int L = levels_for(q);
+  if (!L || n < 1 || n > MPNL_MAX_N) return -1;
+  TreeBuild tb = build_tree(n, L, expansions);
+  if (!tb.ok) return -1;
+  return Workspace(n_vectors, tb.tp.list_bytes, n).total;
+}
 
 int mpnl_plan(const void* h, int h_is_f64, int64_t n_ch, int m, int n, int q, double noise_var,
               int32_t* perm, void* r64, void* qh64, float* tables, void* stream) {
@@ -274,33 +265,88 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   const int64_t B = n_ch * v_per_ch;
   if (n_ch < 0 || v_per_ch < 0) return fail(MPNL_EINVAL, "negative batch");
   if (B == 0) return MPNL_OK;
-  if (workspace_bytes < mpnl_workspace_bytes(B)) return fail(MPNL_EINVAL, "workspace too small");
+  if (B > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "more than 2^31 vectors per call");
   TreeBuild tb = build_tree(n, L, expansions);
   if (!tb.ok) return fail(MPNL_EINVAL, tb.err);
+  const TreeParams& tp = tb.tp;
+  const Workspace W(B, tp.list_bytes, n);
+  if (workspace_bytes < W.total) return fail(MPNL_EINVAL, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
-  int32_t* count = reinterpret_cast<int32_t*>(workspace);
-  int64_t* list = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(workspace) + 16);
+  char* ws = reinterpret_cast<char*>(workspace);
+  DetectArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.tables = tables;
+  a.y = y;
+  a.y_f64 = y_is_f64;
+  a.perm = perm;
+  a.r64 = (const double2*)r64;
+  a.qh64 = (const double2*)qh64;
+  a.hard = hard;
+  a.metric = metric;
+  a.counters = reinterpret_cast<int32_t*>(ws + W.counters);
+  a.fix_list = reinterpret_cast<int64_t*>(ws + W.fix_list);
+  a.vflag = reinterpret_cast<uint32_t*>(ws + W.vflag);
+  a.vres = reinterpret_cast<float4*>(ws + W.vres);
+  a.vpath = reinterpret_cast<int2*>(ws + W.vpath);
+  a.events = reinterpret_cast<int4*>(ws + W.events);
+  a.lists = reinterpret_cast<uint8_t*>(ws + W.lists);
+  a.zq = reinterpret_cast<float2*>(ws + W.zq);
+  a.stats = g_stats;
+  a.n_ch = n_ch;
+  a.V = v_per_ch;
+  a.m = m;
+  a.ev_cap = (int)W.ev_cap;
+  a.metric_offset = m > n;
+  a.guard_scale = (float)(g_guard_scale > 0 ? g_guard_scale : 1.0);
+  // overloaded channels and trees with more than MPNL_XMAX expanded layers
+  // (e.g. full enumeration) are detected entirely by the fp64 kernel
   const bool augmented = n > m;
-  if (stage == 1) {
-    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+  const bool slow = augmented || tp.n_top > MPNL_XMAX;
+  cudaError_t e = cudaSuccess;
+  if (stage == 1) {   // reset + partial-layer selection
+    e = cudaMemsetAsync(a.counters, 0, 16, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.vflag, 0, 4 * B, st);
     if (e != cudaSuccess) return cuda_fail(e, "memset");
-    if (augmented) return MPNL_OK;   // overloaded channels: all vectors go to the fp64 kernel
-    Launch l;
-    std::string err;
-    if (!plan_launch(n, m, L, n_ch, v_per_ch, tb.tp, l, err)) return fail(MPNL_EUNSUPPORTED, err);
-    l.a.tables = tables;
-    l.a.y = y;
-    l.a.y_f64 = y_is_f64;
-    l.a.perm = perm;
-    l.a.hard = hard;
-    l.a.metric = metric;
-    l.a.flags = flags;
-    l.a.flag_count = count;
-    l.a.flag_list = list;
-    e = launch_traverse(n, L, l, tb.tp, st);
-    if (e != cudaSuccess) return cuda_fail(e, "traverse kernel");
+    if (slow) return MPNL_OK;
+    for (int pos = n - 1; pos >= n - tp.n_top; --pos) {
+      if (tp.e[pos] == L * L) continue;
+      const int64_t items = B * (tp.n_paths / tp.stride[pos + 1]);
+      if (items > 0x7fffffffLL * 128) return fail(MPNL_EUNSUPPORTED, "selection grid too large");
+      e = launch_fast(n, L, 0, a, tp, (unsigned)((items + 127) / 128), 128, 0, pos, st);
+      if (e != cudaSuccess) return cuda_fail(e, "select kernel");
+    }
     return MPNL_OK;
   }
+  if (stage == 2 || stage == 3) {
+    if (slow) return MPNL_OK;
+    const int pt = trav_pt(n), S = 32 * pt, P = tp.n_paths;
+    int vpi = 1, bpv = 1;
+    if (P < S && S % P == 0) vpi = std::min(S / P, MPNL_VPI_MAX);
+    else bpv = (P + S - 1) / S;
+    a.vpi = vpi;
+    a.bpv = bpv;
+    const int threads = 128, warps = threads / 32;
+    // vectors per CTA: 4 work items per warp (many small CTAs keep every SM fed;
+    // the per-CTA table staging is a few KB)
+    const int unit = (bpv > 1 || vpi == 1 ? 1 : vpi) * warps;
+    int64_t vc = std::min<int64_t>(4 * unit, v_per_ch);
+    const int64_t chunks = (v_per_ch + vc - 1) / vc;
+    if (n_ch * chunks > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
+    a.vc = (int)vc;
+    a.chunks = (int)chunks;
+    if (stage == 2) {
+      const TravSmem so(m, n, warps);
+      e = launch_fast(n, L, 1, a, tp, (unsigned)(n_ch * chunks), threads, so.total_bytes, 0, st);
+      if (e != cudaSuccess) return cuda_fail(e, "traverse kernel");
+    } else {
+      // first vb blocks: one thread per vector; as many again for the events
+      const int64_t vb = (B + 127) / 128;
+      e = launch_fast(n, L, 2, a, tp, (unsigned)(2 * vb), 128, 0, (int)vb, st);
+      if (e != cudaSuccess) return cuda_fail(e, "verify kernel");
+    }
+    return MPNL_OK;
+  }
+  // stage 4: fp64 fix-up of the listed vectors (or of every vector on the slow path)
   ExactArgs ea;
   std::memset(&ea, 0, sizeof(ea));
   ea.r64 = (const double2*)r64;
@@ -318,18 +364,21 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   ea.hard = hard;
   ea.metric = metric;
   int grid;
-  if (augmented) {
+  if (slow) {
     ea.list = nullptr;
     ea.n_tasks = B;
     grid = (int)std::min<int64_t>((B + 3) / 4, 148 * 16);
-    if (flags) cudaMemsetAsync(flags, 1, B, st);
   } else {
-    ea.list = list;
-    ea.count = count;
+    ea.list = a.fix_list;
+    ea.count = a.counters;
     grid = (int)std::min<int64_t>((B + 3) / 4, 148 * 4);
   }
-  cudaError_t e = launch_exact(ea, tb.tp, grid, st);
+  e = launch_exact(ea, tp, grid, st);
   if (e != cudaSuccess) return cuda_fail(e, "exact kernel");
+  if (flags) {
+    e = launch_flags(flags, a.vflag, B, slow ? 1 : 0, st);
+    if (e != cudaSuccess) return cuda_fail(e, "flags kernel");
+  }
   return MPNL_OK;
 }
 
@@ -338,13 +387,13 @@ int mpnl_detect_hard(const int32_t* perm, const void* r64, const void* qh64, con
                      int q, const int64_t* expansions, double noise_var, uint8_t* hard,
                      float* metric, uint8_t* flags, void* workspace, int64_t workspace_bytes,
                      void* stream) {
-  int rc = mpnl_detect_hard_stage(1, perm, r64, qh64, tables, y, y_is_f64, n_ch, v_per_ch, m, n,
-                                  q, expansions, noise_var, hard, metric, flags, workspace,
-                                  workspace_bytes, stream);
-  if (rc) return rc;
-  return mpnl_detect_hard_stage(2, perm, r64, qh64, tables, y, y_is_f64, n_ch, v_per_ch, m, n, q,
-                                expansions, noise_var, hard, metric, flags, workspace,
-                                workspace_bytes, stream);
+  for (int stage = 1; stage <= 4; ++stage) {
+    const int rc = mpnl_detect_hard_stage(stage, perm, r64, qh64, tables, y, y_is_f64, n_ch,
+                                          v_per_ch, m, n, q, expansions, noise_var, hard, metric,
+                                          flags, workspace, workspace_bytes, stream);
+    if (rc) return rc;
+  }
+  return MPNL_OK;
 }
 
 int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64, const void* y,

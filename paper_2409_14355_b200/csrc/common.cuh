@@ -22,9 +22,9 @@ namespace mpnl {
 // --------------------------------------------------------------------------
 struct TableLayout {
   int m, n;
-  int off_qh;     // N x M float2  : rows of Q^H (fp32), for z = Q^H y
+  int off_qh;     // M x N float2  : Q^H transposed (fp32): qhT[r][k], for z = Q^H y
   int off_shift;  // N float2      : constant symbol offset folded into z
-  int off_lay;    // N float4      : per layer (kneg, c2r, guard_a, unused)
+  int off_lay;    // N float4      : per layer (kneg, c2r, S_k, |shift_k|)
   int off_rcol;   // N x NP float2 : column pos holds r''[k][pos], k < pos
   int np_;        // column stride (N rounded up to even, for 128-bit loads)
   int total;      // floats per channel
@@ -49,8 +49,17 @@ struct TreeParams {
   int stride[MPNL_MAX_N + 1];  // prod_{j<pos} e_j (stride[N] = P)
   int list_off[MPNL_MAX_N];    // byte offset of the partial-layer list (per vector)
   int list_bytes;              // total list bytes per vector
-  int stair_cnt[MPNL_MAX_N];   // staircase(e+1) candidate count for partial layers
+  unsigned ms[MPNL_MAX_N];     // magic for p / stride[pos]   (fast_div)
+  unsigned me[MPNL_MAX_N];     // magic for d / e[pos]
 };
+
+// floor(p / d) for p < 2^24 with m = floor((2^32 - 1) / d): the umulhi estimate
+// is exact or one short; one upward correction makes it exact.
+__host__ __device__ inline unsigned div_magic(unsigned d) { return 0xffffffffu / d; }
+__device__ __forceinline__ unsigned fast_div(unsigned p, unsigned d, unsigned m) {
+  unsigned q = __umulhi(p, m);
+  return q + ((q + 1) * d <= p ? 1u : 0u);
+}
 
 __host__ __device__ inline float qam_norm(int L) {
   // sqrt(2 (L^2 - 1) / 3): 4-QAM sqrt(2), 16-QAM sqrt(10), 64-QAM sqrt(42)

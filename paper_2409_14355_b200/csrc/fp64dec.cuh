@@ -1,0 +1,51 @@
+// fp64 decision helpers with the reference's tie rules, shared by the exact
+// kernel and the event checks of the traversal kernel.
+//   * nearest point for e = 1: the 2-D argmin of |c - s|^2 with the first
+//     (lowest) label on ties (detect.py:418-419 argsort(kind="stable")[0]);
+//     for square QAM it factorises per axis, ties -> lower Gray label.
+//   * the e nearest points: stable order by (|c - s|^2, label).
+#pragma once
+#include "common.cuh"
+
+namespace mpnl {
+
+__device__ __forceinline__ double level_value(int i, int L, double nrm) {
+  return (double)(L - 1 - 2 * i) / nrm;
+}
+
+static __device__ __noinline__ int nearest_level_f64(double c, int L, double nrm) {
+  double bd = 1e300;
+  int bg = 1 << 30, bi = 0;
+  for (int i = 0; i < L; ++i) {
+    const double d = (c - level_value(i, L, nrm)) * (c - level_value(i, L, nrm));
+    const int g = gray_code(i);
+    if (d < bd || (d == bd && g < bg)) { bd = d; bg = g; bi = i; }
+  }
+  return bi;
+}
+
+// 64-bit mask (bit = i*L + j over level indices) of the e nearest points.
+static __device__ __noinline__ unsigned long long nearest_set_f64(double cr, double ci, int L, double nrm,
+                                                     int e) {
+  const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
+  const int Q = L * L;
+  unsigned long long mask = 0ull;
+  for (int q = 0; q < Q; ++q) {
+    const int i = q / L, j = q % L;
+    const double dr = cr - level_value(i, L, nrm), di = ci - level_value(j, L, nrm);
+    const double d = dr * dr + di * di;
+    const int lb = (gray_code(i) << h) | gray_code(j);
+    int rank = 0;
+    for (int q2 = 0; q2 < Q; ++q2) {
+      const int i2 = q2 / L, j2 = q2 % L;
+      const double er = cr - level_value(i2, L, nrm), ei = ci - level_value(j2, L, nrm);
+      const double d2 = er * er + ei * ei;
+      const int lb2 = (gray_code(i2) << h) | gray_code(j2);
+      rank += (d2 < d) || (d2 == d && lb2 < lb);
+    }
+    if (rank < e) mask |= 1ull << q;
+  }
+  return mask;
+}
+
+}  // namespace mpnl

@@ -157,7 +157,7 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
   const double sc = 2.0 / nrm;
   const double lv = (double)(L - 1) / nrm;
   for (int idx = lane; idx < n * m; idx += 32) {
-    int k = idx / m, r = idx % m;
+    int r = idx / n, k = idx % n;       // transposed: qhT[r][k] = conj(q_k[r])
     double2 q = A[r * n + phys_of[k]];
     tc[tl.off_qh + 2 * idx] = (float)q.x;
     tc[tl.off_qh + 2 * idx + 1] = (float)(-q.y);
@@ -173,12 +173,12 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     tc[tl.off_rcol + 2 * idx + 1] = v.y;
   }
   for (int k = lane; k < n; k += 32) {
-    double sr = 0.0, si = 0.0, ga = 0.0;
+    double sr = 0.0, si = 0.0, sabs = 0.0;
     for (int j = k; j < n; ++j) {
       double2 r = Rp[k * n + phys_of[j]];
       sr += r.x;
       si += r.y;
-      if (j > k) ga += sc * sqrt(r.x * r.x + r.y * r.y);
+      if (j > k) sabs += (double)fabsf((float)(sc * r.x)) + (double)fabsf((float)(sc * r.y));
     }
     // shift = (L-1)(1+i)/norm * sum_{j>=k} r_kj
     double shr = lv * (sr - si), shi = lv * (sr + si);
@@ -189,8 +189,9 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     float* ly = tc + tl.off_lay + 4 * k;
     ly[0] = (float)(-1.0 / (c2r * (L - 1)));
     ly[1] = (float)c2r;
-    ly[2] = (float)(sqrt(shr * shr + shi * shi) + (L - 1) * 1.4142135623730951 * ga);
-    ly[3] = 0.f;
+    // guard inputs: S_k = sum_{j>k} |Re r''| + |Im r''| (as stored) and |shift_k|
+    ly[2] = (float)(sabs * (1.0 + 1e-6));
+    ly[3] = (float)(fmax(fabs(shr), fabs(shi)) * (1.0 + 1e-6));
   }
 }
 

@@ -1,4 +1,4 @@
-// K2+K3+K4 — fp32 parallel-path traversal with in-kernel argmin (hard output).
+// K2 + K3 + K4 — the fp32 hard-output fast path, as three uniform kernels.
 //
 // Reference semantics (`/root/reference/pkg/src/mpnlsim/detect.py`):
 //   z = Q^H y                                   detect.py:481
@@ -9,112 +9,86 @@
 //   best = argmin (metric, labels[0], ...)      detect.py:465-470
 //   hard = labels[best] in stream order         cli.py:239, detect.py:431-437
 //
-// B200 design (one CTA = one resource-block channel x a chunk of Vc vectors):
-//   phase A  stage the channel's fp32 tables + the chunk's y in shared memory,
-//            rotate z' = Q^H y - shift (fp32), per-chunk guard thresholds;
-//   phase B  per (vector, parent) selection lists for *partial* expansion
-//            layers (e < Q): e nearest of Q by a staircase rank over the
-//            per-axis Schnorr-Euchner orders (only the SET matters for hard
-//            output; the cut margin is guarded);
-//   phase C  lane = path, PT paths per lane: every path is an independent
-//            SIC chain.  Symbols are level indices held as exact small floats,
-//            the interference of each decided symbol is pushed into the
-//            per-row accumulators (4 FFMA per row, r'' broadcast from smem by
-//            128-bit loads shared by PT paths), slicing is FMUL.SAT + a
-//            magic-number round, the partial Euclidean distance accumulates
-//            in registers.  Warp-shuffle argmin over paths on (metric, path);
-//   phase D  one thread per vector re-traces its winning path with the very
-//            same arithmetic (bit-identical), writes Gray labels in stream
-//            order + the metric, and raises a flag when a guarded decision
-//            on a competitive path or a near-tie could differ from fp64.
-// Flagged vectors are recomputed by the fp64 kernel (exact.cu).
+// select_kernel   (K2, only for partial layers 1 < e < Q) one thread per
+//                 (vector, parent): the e nearest points by a k-smallest-sum
+//                 merge of the two per-axis Schnorr-Euchner orders (only the SET
+//                 matters for hard output); a cut closer than the fp32 error
+//                 bound is logged as an event.
+// traverse_kernel (K3, the hot kernel) CTA = a channel's chunk of vectors; the
+//                 channel's tables are staged in shared memory once, then every
+//                 warp loops over its vectors with no block barrier: rotate
+//                 z' = Q^H y - shift (lane = row), per-vector per-layer fp32
+//                 error bounds, then lane = path (PT paths per lane): each path
+//                 is an independent SIC chain; symbols are level indices held as
+//                 exact small floats, each decided symbol is pushed into the
+//                 per-row accumulators (4 FFMA per row; one 128-bit LDS of r''
+//                 serves 2 rows x PT paths), slicing = FMUL.SAT + magic-number
+//                 round, the PED accumulates in registers.  A decision closer to
+//                 a boundary than the bound sets a bit in a per-path mask
+//                 (branch-free); paths with a competitive marked decision are
+//                 logged.  Top-3 (metric, path) per vector with warp REDUX.
+// verify_kernel   (K4) thread per vector: re-trace the winner with the very same
+//                 arithmetic (bit-identical), write Gray labels in stream order;
+//                 settle a 2-way near-tie in fp64.  Thread per logged event:
+//                 re-decide the marked decisions of competitive paths in fp64
+//                 from the path's own prefix.  Disagreements, 3-way ties and
+//                 overflows go to the fp64 kernel (exact.cu).
 #pragma once
 #include "common.cuh"
+#include "fp64dec.cuh"
 
 namespace mpnl {
 
-struct TraverseArgs {
-  const float* tables;      // per channel blob (TableLayout)
+struct DetectArgs {
+  const float* tables;      // (n_ch, T) per channel blob (TableLayout)
   const void* y;            // (n_ch, V, M) complex64 or complex128
   const int32_t* perm;      // (n_ch, N)
-  uint8_t* hard;            // (n_ch, V, N) Gray labels, stream order
-  float* metric;            // (n_ch, V)
-  uint8_t* flags;           // (n_ch, V) or null
-  int32_t* flag_count;      // device counter
-  int64_t* flag_list;       // global vector indices needing fp64 recompute
+  const double2* r64;       // (n_ch, N, N)
+  const double2* qh64;      // (n_ch, N, M)
+  uint8_t* hard;            // (B, N) Gray labels, stream order
+  float* metric;            // (B,)
+  // workspace
+  int32_t* counters;        // [0] fix-up count, [1] event count
+  int64_t* fix_list;        // (B,) vectors for the fp64 kernel
+  uint32_t* vflag;          // (B,) 1 = sent to fp64
+  float4* vres;             // (B,) b1, b2, b3, E_acc (L2)
+  int2* vpath;              // (B,) p1, p2
+  int4* events;             // (ev_cap,) {path, mask|pos, vector, type}
+  uint8_t* lists;           // (B, list_bytes) partial-layer selections
+  float2* zq;               // (B, N) z' as computed by the traversal kernel
+  int32_t* stats;           // diagnostics (may be null)
   int64_t n_ch, V;
   int m;
   int y_f64;
-  int vc;                   // vectors per CTA chunk
-  int chunks;               // chunks per channel
-  int vpi;                  // vectors per work item (VPI mode) or 1
-  int bpv;                  // path batches per vector (batch mode) or 1
-  int has_partial;          // any partial expansion layer (phase B needed)
+  int ev_cap;
+  int vc, chunks;           // traverse: vectors per CTA, chunks per channel
+  int vpi, bpv;             // vectors per warp item (VPI mode) / path batches per vector
   int metric_offset;        // 1 when M > N: add ||y||^2 - ||z||^2
-  float tau;                // guard: relative fp32 error scale
+  float guard_scale;        // scales the fp32 error bound (1 = rigorous)
 };
 
-#define MPNL_GROUP 8          // lanes per phase-B item
-#define MPNL_GSCR 96          // floats of phase-B scratch per group
-#define MPNL_MAGIC 8388608.0f // 2^23: fma(a, L-1, 2^23) rounds a to an integer
+#define MPNL_XMAX 3             // expanded (e > 1) layers handled by the fast path
+#define MPNL_VPI_MAX 8          // vectors per warp item in VPI mode
+#define MPNL_MAGIC 8388608.0f   // 2^23: fma(a, L-1, 2^23) rounds a to an integer
+#define MPNL_U 5.9604645e-08f   // 2^-24
+#define EV_NODE 0
+#define EV_CUT 1
+#define TRAV_EV_CAP 256         // per-CTA event buffer of the traversal kernel
 
-// shared-memory carve-up (offsets in floats; lists in bytes), host == device
-struct TravSmem {
-  int tab, y, z, thr, vb1, vb2, vfm, vbp, vcorr, misc, gscr, lists, total_bytes;
-  __host__ __device__ TravSmem(int m, int n, int vc, int list_bytes, int ngroups) {
-    TableLayout tl(m, n);
-    int o = 0;
-    tab = o; o += tl.total;
-    y = o; o += TableLayout::up4(2 * vc * m);
-    z = o; o += TableLayout::up4(2 * vc * n);
-    thr = o; o += TableLayout::up4(n);
-    vb1 = o; o += TableLayout::up4(vc);
-    vb2 = o; o += TableLayout::up4(vc);
-    vfm = o; o += TableLayout::up4(vc);
-    vbp = o; o += TableLayout::up4(vc);
-    vcorr = o; o += TableLayout::up4(vc);
-    misc = o; o += 4;                        // [0] max ||y||, [1] E_acc max
-    gscr = o; o += ngroups * MPNL_GSCR;
-    lists = o * 4;
-    total_bytes = lists + ((vc * list_bytes + 15) & ~15);
-  }
-};
+// ---------------------------------------------------------------------------
+// arithmetic shared by all kernels: keeping it in one place makes the
+// re-traces bit-identical to the traversal.
+// ---------------------------------------------------------------------------
 
-struct Best {
-  float b1, b2, fm;
-  int bp;
-};
-
-__device__ __forceinline__ Best best_merge(Best a, Best b) {
-  Best r;
-  if (b.b1 < a.b1 || (b.b1 == a.b1 && b.bp < a.bp)) {
-    r.b1 = b.b1; r.bp = b.bp; r.b2 = fminf(a.b1, b.b2);
-  } else {
-    r.b1 = a.b1; r.bp = a.bp; r.b2 = fminf(a.b2, b.b1);
-  }
-  r.fm = fminf(a.fm, b.fm);
-  return r;
-}
-
-__device__ __forceinline__ Best best_shfl(Best a, int off) {
-  Best o;
-  o.b1 = __shfl_xor_sync(0xffffffffu, a.b1, off);
-  o.b2 = __shfl_xor_sync(0xffffffffu, a.b2, off);
-  o.fm = __shfl_xor_sync(0xffffffffu, a.fm, off);
-  o.bp = __shfl_xor_sync(0xffffffffu, a.bp, off);
-  return best_merge(a, o);
-}
-
-// Level indices of path p's symbol at an expanded layer pos.
 template <int L>
 __device__ __forceinline__ void expanded_symbol(const TreeParams& tp, int pos, int p,
                                                 const uint8_t* vlist, int& ir, int& ii) {
-  const int e = tp.e[pos];
-  const int d = p / tp.stride[pos];
-  if (e == L * L) {
-    const int dd = d % e;          // full layer: any digit -> point bijection
-    ir = dd / L;
-    ii = dd - ir * L;
+  const unsigned e = (unsigned)tp.e[pos];
+  const unsigned d = fast_div((unsigned)p, (unsigned)tp.stride[pos], tp.ms[pos]);
+  if (e == (unsigned)(L * L)) {
+    const unsigned dd = d - fast_div(d, e, tp.me[pos]) * e;   // full layer: digit -> point
+    ir = (int)(dd / L);
+    ii = (int)(dd % L);
   } else {
     const uint8_t b = vlist[tp.list_off[pos] + d];
     ir = b >> 3;
@@ -122,22 +96,104 @@ __device__ __forceinline__ void expanded_symbol(const TreeParams& tp, int pos, i
   }
 }
 
-// One traversal of NS independent paths (tab = the channel's table blob in smem).
-// GUARD: keep the PED prefix of any near-boundary decision in fped.
-// LAB:   capture level indices (ir*8+ii) per position (NS must be 1).
-template <int N, int L, int NS, bool GUARD, bool LAB>
-__device__ __forceinline__ void traverse_paths(const float* __restrict__ tab,
-                                               const float2* __restrict__ zs,
+// slice one axis: a' = sat(acc * kneg), i = round(a' (L-1)); t = a'(L-1) - i
+template <int L>
+__device__ __forceinline__ float slice_axis(float acc, float kneg, float& t) {
+  const float s = __saturatef(__fmul_rn(acc, kneg));
+  const float mm = __fmaf_rn(s, (float)(L - 1), MPNL_MAGIC);
+  const float f = __fsub_rn(mm, MPNL_MAGIC);
+  t = __fmaf_rn(s, (float)(L - 1), -f);
+  return f;
+}
+
+__device__ __forceinline__ float ped_step(float ped, float c2r, float fr, float fi, float ur,
+                                          float ui) {
+  const float er = __fmaf_rn(c2r, fr, ur);
+  const float ei = __fmaf_rn(c2r, fi, ui);
+  ped = __fmaf_rn(er, er, ped);
+  return __fmaf_rn(ei, ei, ped);
+}
+
+__device__ __forceinline__ void acc_step(float& ar, float& ai, float rr, float ri, float fr,
+                                         float fi) {
+  ar = __fmaf_rn(rr, fr, ar);
+  ar = __fmaf_rn(-ri, fi, ar);
+  ai = __fmaf_rn(rr, fi, ai);
+  ai = __fmaf_rn(ri, fr, ai);
+}
+
+__device__ __forceinline__ float2 load_y32(const DetectArgs& a, int64_t idx) {
+  if (a.y_f64) {
+    const double2 v = reinterpret_cast<const double2*>(a.y)[idx];
+    return make_float2((float)v.x, (float)v.y);
+  }
+  return reinterpret_cast<const float2*>(a.y)[idx];
+}
+
+// z'_k = (Q^H y)_k - shift_k in fp32 (identical sequence everywhere)
+template <typename YF>
+__device__ __forceinline__ float2 rotate_row(const float* tab, int m, int n, int k, YF yat) {
+  const TableLayout tl(m, n);
+  const float2* qt = reinterpret_cast<const float2*>(tab + tl.off_qh);
+  float zr = 0.f, zi = 0.f;
+  for (int r = 0; r < m; ++r) {
+    const float2 q = qt[r * n + k], yv = yat(r);
+    zr = __fmaf_rn(q.x, yv.x, zr);
+    zr = __fmaf_rn(-q.y, yv.y, zr);
+    zi = __fmaf_rn(q.x, yv.y, zi);
+    zi = __fmaf_rn(q.y, yv.x, zi);
+  }
+  const float2 sh = reinterpret_cast<const float2*>(tab + tl.off_shift)[k];
+  return make_float2(__fsub_rn(zr, sh.x), __fsub_rn(zi, sh.y));
+}
+
+// acc-domain fp32 error bound of row k's decision variable:
+//   u [ (2M+1) sqrt2 |y| + |z'_k| + |shift_k| + (2(N-1-k)+1) (|z'_k| + (L-1) S_k) ]
+__device__ __forceinline__ float row_bound(float ynorm, float2 zk, float4 lyk, int k, int m, int n,
+                                           int L, float gs) {
+  const float za = fmaxf(fabsf(zk.x), fabsf(zk.y));
+  const float xk = za + (float)(L - 1) * lyk.z;
+  return gs * MPNL_U * 1.01f *
+         ((2.f * m + 1.f) * 1.4142136f * ynorm + za + lyk.w + (2.f * (n - 1 - k) + 1.f) * xk);
+}
+
+// fp32 PED error bound from the L2 norm of the per-layer acc bounds
+__device__ __forceinline__ float ped_tol(float b, float eacc, int n) {
+  return 2.f * sqrtf(b) * eacc + eacc * eacc + 2.f * n * MPNL_U * b;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct TabPtrs {
+  const float4* lay4;
+  const float* rcol;   // 16-byte aligned columns of NP float2
+};
+
+__device__ __forceinline__ TabPtrs tab_ptrs(const float* tab, int m, int n) {
+  const TableLayout tl(m, n);
+  TabPtrs t;
+  t.lay4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
+  t.rcol = reinterpret_cast<const float*>(__builtin_assume_aligned(tab + tl.off_rcol, 16));
+  return t;
+}
+
+// K3 inner loop: NS independent paths.  Per path: PED, mask of layers whose
+// decision was within the bound, PED prefix at the first such layer.
+template <int N, int L, int NS>
+__device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float2* __restrict__ zs,
                                                const float* __restrict__ thr,
                                                const uint8_t* __restrict__ lists,
                                                const TreeParams& tp, int list_bytes,
-                                               const int (&vl)[NS], const int (&p)[NS],
-                                               float (&ped)[NS], float (&fped)[NS],
-                                               int (&lab)[N], int m) {
+                                               const int (&vl)[NS], const int64_t (&gvl)[NS],
+                                               const int (&p)[NS], float (&ped)[NS],
+                                               unsigned (&evm)[NS], float (&evp)[NS]) {
   constexpr int NP = (N + 1) & ~1;
-  const TableLayout tl(m, N);
-  const float4* lay4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
-  const float* rcol = tab + tl.off_rcol;
+  constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
+  const float INF = __int_as_float(0x7f800000);
   float ar[NS][N], ai[NS][N];
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
@@ -148,417 +204,702 @@ __device__ __forceinline__ void traverse_paths(const float* __restrict__ tab,
       ai[s][k] = z.y;
     }
     ped[s] = 0.f;
-    fped[s] = __int_as_float(0x7f800000);
+    evm[s] = 0u;
+    evp[s] = INF;
   }
-  const int top_lo = N - tp.n_top;   // layers pos >= top_lo are expanded
+  const int top_lo = N - tp.n_top;   // layers pos >= top_lo are expanded (n_top <= XM)
 #pragma unroll
   for (int pos = N - 1; pos >= 0; --pos) {
-    const float4 ly = lay4[pos];
+    const float4 ly = T.lay4[pos];
     const float kneg = ly.x, c2r = ly.y;
     float fr[NS], fi[NS];
-    if (pos >= top_lo) {
+    if (pos >= N - XM && pos >= top_lo) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         int ir, ii;
-        expanded_symbol<L>(tp, pos, p[s], lists + vl[s] * list_bytes, ir, ii);
+        expanded_symbol<L>(tp, pos, p[s], lists + gvl[s] * list_bytes, ir, ii);
         fr[s] = (float)ir;
         fi[s] = (float)ii;
-        if (LAB) lab[pos] = ir * 8 + ii;
       }
     } else {
-      float th = 0.f;
-      if (GUARD) th = thr[pos];
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const float sr = __saturatef(__fmul_rn(ar[s][pos], kneg));
-        const float si = __saturatef(__fmul_rn(ai[s][pos], kneg));
-        const float mr = __fmaf_rn(sr, (float)(L - 1), MPNL_MAGIC);
-        const float mi = __fmaf_rn(si, (float)(L - 1), MPNL_MAGIC);
-        fr[s] = __fsub_rn(mr, MPNL_MAGIC);
-        fi[s] = __fsub_rn(mi, MPNL_MAGIC);
-        if (GUARD) {
-          const float tr = __fmaf_rn(sr, (float)(L - 1), -fr[s]);
-          const float ti = __fmaf_rn(si, (float)(L - 1), -fi[s]);
-          if (fabsf(tr) > th || fabsf(ti) > th) fped[s] = fminf(fped[s], ped[s]);
-        }
-        if (LAB) lab[pos] = (int)fr[s] * 8 + (int)fi[s];
+        const float th = thr[vl[s] * N + pos];
+        float tr, ti;
+        fr[s] = slice_axis<L>(ar[s][pos], kneg, tr);
+        fi[s] = slice_axis<L>(ai[s][pos], kneg, ti);
+        const bool near = fabsf(tr) > th || fabsf(ti) > th;
+        evm[s] |= near ? (1u << pos) : 0u;
+        evp[s] = near ? fminf(evp[s], ped[s]) : evp[s];
       }
     }
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const float er = __fmaf_rn(c2r, fr[s], ar[s][pos]);
-      const float ei = __fmaf_rn(c2r, fi[s], ai[s][pos]);
-      ped[s] = __fmaf_rn(er, er, ped[s]);
-      ped[s] = __fmaf_rn(ei, ei, ped[s]);
-    }
+    for (int s = 0; s < NS; ++s) ped[s] = ped_step(ped[s], c2r, fr[s], fi[s], ar[s][pos], ai[s][pos]);
     // push this layer's symbols into the rows below: acc_k += r''_k,pos * s
-    const float4* rc = reinterpret_cast<const float4*>(rcol + 2 * NP * pos);
+    const float4* rc = reinterpret_cast<const float4*>(T.rcol + 2 * NP * pos);
 #pragma unroll
     for (int k = 0; k < pos; k += 2) {
       const float4 r2 = rc[k >> 1];
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        ar[s][k] = __fmaf_rn(r2.x, fr[s], ar[s][k]);
-        ar[s][k] = __fmaf_rn(-r2.y, fi[s], ar[s][k]);
-        ai[s][k] = __fmaf_rn(r2.x, fi[s], ai[s][k]);
-        ai[s][k] = __fmaf_rn(r2.y, fr[s], ai[s][k]);
-        if (k + 1 < pos) {
-          ar[s][k + 1] = __fmaf_rn(r2.z, fr[s], ar[s][k + 1]);
-          ar[s][k + 1] = __fmaf_rn(-r2.w, fi[s], ar[s][k + 1]);
-          ai[s][k + 1] = __fmaf_rn(r2.z, fi[s], ai[s][k + 1]);
-          ai[s][k + 1] = __fmaf_rn(r2.w, fr[s], ai[s][k + 1]);
-        }
+        acc_step(ar[s][k], ai[s][k], r2.x, r2.y, fr[s], fi[s]);
+        if (k + 1 < pos) acc_step(ar[s][k + 1], ai[s][k + 1], r2.z, r2.w, fr[s], fi[s]);
       }
     }
   }
 }
 
+// Single-path re-trace with the identical arithmetic: level indices lab[pos]
+// (ir*8+ii) and the PED prefix pre[pos] before layer pos, for pos >= stop.
+template <int N, int L>
+__device__ __forceinline__ void retrace_inline(const float* tab, int m, const float2* zs,
+                                               const uint8_t* vlist, const TreeParams& tp, int p,
+                                               int stop, int* lab, float* pre) {
+  constexpr int NP = (N + 1) & ~1;
+  constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
+  const TabPtrs T = tab_ptrs(tab, m, N);
+  float ar[N], ai[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    ar[k] = zs[k].x;
+    ai[k] = zs[k].y;
+  }
+  float ped = 0.f;
+  const int top_lo = N - tp.n_top;
+#pragma unroll
+  for (int pos = N - 1; pos >= 0; --pos) {
+    const float4 ly = T.lay4[pos];
+    float fr, fi;
+    if (pos >= N - XM && pos >= top_lo) {
+      int ir, ii;
+      expanded_symbol<L>(tp, pos, p, vlist, ir, ii);
+      fr = (float)ir;
+      fi = (float)ii;
+    } else {
+      float tr, ti;
+      fr = slice_axis<L>(ar[pos], ly.x, tr);
+      fi = slice_axis<L>(ai[pos], ly.x, ti);
+    }
+    lab[pos] = (int)fr * 8 + (int)fi;
+    pre[pos] = ped;
+    if (pos == stop) return;
+    ped = ped_step(ped, ly.y, fr, fi, ar[pos], ai[pos]);
+    const float4* rc = reinterpret_cast<const float4*>(T.rcol + 2 * NP * pos);
+#pragma unroll
+    for (int k = 0; k < pos; k += 2) {
+      const float4 r2 = rc[k >> 1];
+      acc_step(ar[k], ai[k], r2.x, r2.y, fr, fi);
+      if (k + 1 < pos) acc_step(ar[k + 1], ai[k + 1], r2.z, r2.w, fr, fi);
+    }
+  }
+}
+
+// out-of-line copy for the rare paths (ties, events)
+template <int N, int L>
+static __device__ __noinline__ void retrace_path(const float* tab, int m, const float2* zs,
+                                                 const uint8_t* vlist, const TreeParams& tp, int p,
+                                                 int stop, int* lab, float* pre) {
+  retrace_inline<N, L>(tab, m, zs, vlist, tp, p, stop, lab, pre);
+}
+
 template <int N>
 struct TravCfg {
   static constexpr int PT = N <= 8 ? 4 : 2;              // paths per lane
-  static constexpr int MAXT = N <= 16 ? 256 : 128;       // threads per CTA
-  static constexpr int MINB = 2;                         // CTAs per SM
+  static constexpr int MAXT = 128;                       // threads per CTA
+  static constexpr int MINB = N <= 16 ? 4 : 2;           // CTAs per SM
+};
+
+// ---------------------------------------------------------------------------
+// fp64 helpers (rare paths)
+// ---------------------------------------------------------------------------
+static __device__ __noinline__ void z_f64(const DetectArgs& a, int64_t c, int64_t gv, int n, int k,
+                                          double& zr, double& zi) {
+  // independent loads batched 8 at a time (this runs on latency-bound threads)
+  const double2* QH = a.qh64 + (c * (int64_t)n + k) * a.m;
+  double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
+  const int m = a.m;
+  if (a.y_f64) {
+    const double2* Y = reinterpret_cast<const double2*>(a.y) + gv * m;
+#pragma unroll 8
+    for (int r = 0; r < m; ++r) {
+      const double2 v = __ldg(Y + r), q = __ldg(QH + r);
+      if (r & 1) { ar1 = fma(q.x, v.x, fma(-q.y, v.y, ar1)); ai1 = fma(q.x, v.y, fma(q.y, v.x, ai1)); }
+      else { ar0 = fma(q.x, v.x, fma(-q.y, v.y, ar0)); ai0 = fma(q.x, v.y, fma(q.y, v.x, ai0)); }
+    }
+  } else {
+    const float2* Y = reinterpret_cast<const float2*>(a.y) + gv * m;
+#pragma unroll 8
+    for (int r = 0; r < m; ++r) {
+      const float2 v = __ldg(Y + r);
+      const double2 q = __ldg(QH + r);
+      const double vx = v.x, vy = v.y;
+      if (r & 1) { ar1 = fma(q.x, vx, fma(-q.y, vy, ar1)); ai1 = fma(q.x, vy, fma(q.y, vx, ai1)); }
+      else { ar0 = fma(q.x, vx, fma(-q.y, vy, ar0)); ai0 = fma(q.x, vy, fma(q.y, vx, ai0)); }
+    }
+  }
+  zr = ar0 + ar1;
+  zi = ai0 + ai1;
+}
+
+static __device__ __noinline__ void centre_f64(const DetectArgs& a, int64_t c, int64_t gv, int n,
+                                        int pos, const int* lab, int L, double& cr, double& ci) {
+  const double nrm = qam_norm_d(L);
+  const double2* R = a.r64 + c * (int64_t)n * n;
+  double zr, zi;
+  z_f64(a, c, gv, n, pos, zr, zi);
+  for (int j = n - 1; j > pos; --j) {
+    const double sr = level_value(lab[j] >> 3, L, nrm), si = level_value(lab[j] & 7, L, nrm);
+    const double2 r = R[pos * n + j];
+    zr -= r.x * sr - r.y * si;
+    zi -= r.x * si + r.y * sr;
+  }
+  const double rpp = R[pos * n + pos].x;
+  cr = zr / rpp;
+  ci = zi / rpp;
+}
+
+static __device__ __noinline__ double ped_f64(const DetectArgs& a, int64_t c, int64_t gv, int n,
+                                       const int* lab, int L) {
+  const double nrm = qam_norm_d(L);
+  const double2* R = a.r64 + c * (int64_t)n * n;
+  double acc = 0.0;
+  for (int k = 0; k < n; ++k) {
+    double zr, zi;
+    z_f64(a, c, gv, n, k, zr, zi);
+    for (int j = k; j < n; ++j) {
+      const double sr = level_value(lab[j] >> 3, L, nrm), si = level_value(lab[j] & 7, L, nrm);
+      const double2 r = R[k * n + j];
+      zr -= r.x * sr - r.y * si;
+      zi -= r.x * si + r.y * sr;
+    }
+    acc += zr * zr + zi * zi;
+  }
+  return acc;
+}
+
+// mark vector gv for the fp64 kernel (the first marker appends it to the list)
+__device__ __forceinline__ void send_to_fp64(const DetectArgs& a, int64_t gv) {
+  if (atomicExch(a.vflag + gv, 1u) == 0u) {
+    const int slot = atomicAdd(a.counters, 1);
+    a.fix_list[slot] = gv;
+    if (a.stats) atomicAdd(a.stats + 3, 1);
+  }
+}
+
+__device__ __forceinline__ void log_event(const DetectArgs& a, int4 e) {
+  const int idx = atomicAdd(a.counters + 1, 1);
+  if (idx < a.ev_cap) a.events[idx] = e;
+  else send_to_fp64(a, (int64_t)(unsigned)e.z);
+}
+
+// ---------------------------------------------------------------------------
+// top-3 (metric, path) bookkeeping
+// ---------------------------------------------------------------------------
+struct Top3 {
+  float m1, m2, m3;
+  unsigned p1, p2;
+};
+
+__device__ __forceinline__ bool tless(float a, unsigned pa, float b, unsigned pb) {
+  return a < b || (a == b && pa < pb);
+}
+
+__device__ __forceinline__ void top3_insert(Top3& t, float m, unsigned p) {
+  if (tless(m, p, t.m1, t.p1)) {
+    t.m3 = t.m2; t.m2 = t.m1; t.p2 = t.p1; t.m1 = m; t.p1 = p;
+  } else if (tless(m, p, t.m2, t.p2)) {
+    t.m3 = t.m2; t.m2 = m; t.p2 = p;
+  } else {
+    t.m3 = fminf(t.m3, m);
+  }
+}
+
+__device__ __forceinline__ void top3_pop(Top3& t) {
+  t.m1 = t.m2; t.p1 = t.p2; t.m2 = t.m3; t.p2 = 0xffffffffu;
+  t.m3 = __int_as_float(0x7f800000);
+}
+
+// warp-wide three smallest (metric, path) (metrics >= 0 order like uints: REDUX.MIN)
+__device__ __forceinline__ void warp_top3(Top3 t, float& b1, unsigned& q1, float& b2,
+                                          unsigned& q2, float& b3) {
+  unsigned k = __reduce_min_sync(0xffffffffu, __float_as_uint(t.m1));
+  unsigned q = __reduce_min_sync(0xffffffffu, __float_as_uint(t.m1) == k ? t.p1 : 0xffffffffu);
+  b1 = __uint_as_float(k);
+  q1 = q;
+  if (__float_as_uint(t.m1) == k && t.p1 == q) top3_pop(t);
+  k = __reduce_min_sync(0xffffffffu, __float_as_uint(t.m1));
+  q = __reduce_min_sync(0xffffffffu, __float_as_uint(t.m1) == k ? t.p1 : 0xffffffffu);
+  b2 = __uint_as_float(k);
+  q2 = q;
+  if (__float_as_uint(t.m1) == k && t.p1 == q) top3_pop(t);
+  b3 = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(t.m1)));
+}
+
+// shuffle-based variant for groups of `width` < 32 lanes (VPI mode)
+__device__ __forceinline__ void group_top3(Top3 t, int width, float& b1, unsigned& q1, float& b2,
+                                           unsigned& q2, float& b3) {
+  for (int o = width >> 1; o; o >>= 1) {
+    Top3 u;
+    u.m1 = __shfl_xor_sync(0xffffffffu, t.m1, o);
+    u.m2 = __shfl_xor_sync(0xffffffffu, t.m2, o);
+    u.m3 = __shfl_xor_sync(0xffffffffu, t.m3, o);
+    u.p1 = __shfl_xor_sync(0xffffffffu, t.p1, o);
+    u.p2 = __shfl_xor_sync(0xffffffffu, t.p2, o);
+    Top3 r = t;
+    top3_insert(r, u.m1, u.p1);
+    top3_insert(r, u.m2, u.p2);
+    r.m3 = fminf(r.m3, u.m3);
+    t = r;
+  }
+  b1 = t.m1; q1 = t.p1; b2 = t.m2; q2 = t.p2; b3 = t.m3;
+}
+
+// ===========================================================================
+// K2: partial-layer selection lists, one thread per (vector, parent)
+// ===========================================================================
+template <int N, int L>
+__global__ void __launch_bounds__(128)
+select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
+  constexpr int NP = (N + 1) & ~1;
+  constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
+  __shared__ TreeParams tp;
+  __shared__ float scratch[20 * 128];
+  {
+    const int* s = reinterpret_cast<const int*>(&tparam);
+    int* d = reinterpret_cast<int*>(&tp);
+    for (int i = threadIdx.x; i < (int)(sizeof(TreeParams) / 4); i += blockDim.x) d[i] = s[i];
+  }
+  __syncthreads();
+  const float INF = __int_as_float(0x7f800000);
+  const int m = a.m;
+  const TableLayout tl(m, N);
+  const int e = tp.e[pos];
+  const int npar = tp.n_paths / tp.stride[pos + 1];
+  const int64_t B = a.n_ch * a.V;
+  const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= B * npar) return;
+  const int64_t gv = item / npar;
+  const int par = (int)(item - gv * npar);
+  const int64_t c = gv / a.V;
+  const float* tab = a.tables + c * (int64_t)tl.total;
+  const TabPtrs T = tab_ptrs(tab, m, N);
+  const int p0 = par * tp.stride[pos + 1];
+  uint8_t* vlist = a.lists + gv * tp.list_bytes;
+  auto yat = [&](int r) { return load_y32(a, gv * m + r); };
+  // prefix symbols (expanded layers above pos)
+  float sr[XM], si[XM];
+#pragma unroll
+  for (int q = 0; q < XM; ++q) {
+    const int j = N - 1 - q;
+    sr[q] = 0.f; si[q] = 0.f;
+    if (j > pos) {
+      int ir, ii;
+      expanded_symbol<L>(tp, j, p0, vlist, ir, ii);
+      sr[q] = (float)ir; si[q] = (float)ii;
+    }
+  }
+  // acc at each prefix layer and at pos (traversal order), PED prefix
+  float pedp = 0.f, xr = 0.f, xi = 0.f;
+  float2 zpos = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int q = 0; q < XM; ++q) {
+    const int j = N - 1 - q;
+    if (j < pos) break;
+    const float2 zj = rotate_row(tab, m, N, j, yat);
+    float ar_ = zj.x, ai_ = zj.y;
+#pragma unroll
+    for (int q2 = 0; q2 < q; ++q2) {
+      const int l = N - 1 - q2;
+      const float2 r2 = reinterpret_cast<const float2*>(T.rcol + 2 * NP * l)[j];
+      acc_step(ar_, ai_, r2.x, r2.y, sr[q2], si[q2]);
+    }
+    if (j > pos) pedp = ped_step(pedp, T.lay4[j].y, sr[q], si[q], ar_, ai_);
+    else { xr = ar_; xi = ai_; zpos = zj; }
+  }
+  (void)pedp;
+  // error bound of the centre (index units) for the cut guard
+  float yn = 0.f;
+  for (int r = 0; r < m; ++r) {
+    const float2 v = yat(r);
+    yn = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, yn));
+  }
+  const float4 lyp = T.lay4[pos];
+  const float E = row_bound(sqrtf(yn) * 1.0001f, zpos, lyp, pos, m, N, L, a.guard_scale) / lyp.y +
+                  MPNL_U * 2.f * L;
+  // centre in level-index units (unclamped)
+  const float cx = __fmul_rn(__fmul_rn(xr, lyp.x), (float)(L - 1));
+  const float cy = __fmul_rn(__fmul_rn(xi, lyp.x), (float)(L - 1));
+  // per-axis closest-first level orders in a transposed per-thread scratch
+  const int nth = blockDim.x;
+  float* scr = scratch + threadIdx.x;
+  uint8_t* sox = reinterpret_cast<uint8_t*>(scr + 16 * nth);
+  uint8_t* soy = reinterpret_cast<uint8_t*>(scr + 18 * nth);
+#pragma unroll
+  for (int ax = 0; ax < 2; ++ax) {
+    const float x = ax ? cy : cx;
+    const int n0 = (int)rintf(fminf(fmaxf(x, 0.f), (float)(L - 1)));
+    int lo = n0 - 1, hi = n0 + 1;
+    float* dd = scr + (ax ? 8 : 0) * nth;
+    uint8_t* oo = ax ? soy : sox;
+    oo[0] = (uint8_t)n0;
+    dd[0] = (x - n0) * (x - n0);
+#pragma unroll
+    for (int r = 1; r < L; ++r) {
+      const bool up = (hi < L) && (lo < 0 || (hi - x) < (x - lo));
+      const int lev = up ? hi : lo;
+      hi += up ? 1 : 0;
+      lo -= up ? 0 : 1;
+      oo[(r & 3) + (r >> 2) * 4 * nth] = (uint8_t)lev;
+      dd[r * nth] = (x - lev) * (x - lev);
+    }
+  }
+  auto ldx = [&](int i) { return scr[i * nth]; };
+  auto ldy = [&](int j) { return scr[(8 + j) * nth]; };
+  auto lox = [&](int i) { return (int)sox[(i & 3) + (i >> 2) * 4 * nth]; };
+  auto loy = [&](int j) { return (int)soy[(j & 3) + (j >> 2) * 4 * nth]; };
+  // k-smallest sums dx[i] + dy[w_i] (rows sorted): e members + the (e+1)-th
+  int w[L];
+  float nk[L];
+  const float dy0 = ldy(0);
+#pragma unroll
+  for (int i = 0; i < L; ++i) { w[i] = 0; nk[i] = ldx(i) + dy0; }
+  float kprev = 0.f, knext = 0.f;
+  uint8_t* out = vlist + tp.list_off[pos] + par * e;
+  for (int pick = 0; pick <= e; ++pick) {
+    int sel = 0, col = w[0];
+    float best = nk[0];
+#pragma unroll
+    for (int i = 1; i < L; ++i)
+      if (nk[i] < best) { best = nk[i]; sel = i; col = w[i]; }
+    if (pick < e) { out[pick] = (uint8_t)((lox(sel) << 3) | loy(col)); kprev = best; }
+    else knext = best;
+    const float nxt = (col + 1 < L) ? ldx(sel) + ldy(col + 1) : INF;
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+      if (i == sel) { w[i] = col + 1; nk[i] = nxt; }
+  }
+  // cut guard: distance keys are within 2 sqrt2 E (sqrt k) + 2E^2 (+ rounding)
+  const float bound = 2.8284272f * E * (sqrtf(kprev) + sqrtf(knext)) + 4.f * E * E +
+                      8.f * MPNL_U * (knext + 1.f);
+  if (knext - kprev <= bound) log_event(a, make_int4(p0, pos, (int)gv, EV_CUT));
+}
+
+// ===========================================================================
+// K3: traversal (hot kernel)
+// ===========================================================================
+struct TravSmem {
+  int tpo, tab, wz, wthr, wy, ev, evn, total_bytes;
+  __host__ __device__ TravSmem(int m, int n, int warps) {
+    TableLayout tl(m, n);
+    int o = 0;
+    tpo = o; o += TableLayout::up4((int)(sizeof(TreeParams) / 4));
+    tab = o; o += tl.total;
+    wz = o; o += warps * 2 * MPNL_VPI_MAX * n;     // per warp z' (VPI x N float2)
+    wthr = o; o += warps * MPNL_VPI_MAX * n;       // per warp thresholds
+    wy = o; o += warps * 2 * MPNL_MAX_M;           // per warp y (float2)
+    ev = o; o += 4 * TRAV_EV_CAP;                  // int4 event buffer
+    evn = o; o += 4;
+    total_bytes = o * 4;
+  }
 };
 
 template <int N, int L>
 __global__ void __launch_bounds__(TravCfg<N>::MAXT, TravCfg<N>::MINB)
-traverse_kernel(const TraverseArgs a, const TreeParams tp) {
+traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   constexpr int PT = TravCfg<N>::PT;
   constexpr int S = 32 * PT;
   extern __shared__ __align__(16) float sm[];
-  const int ngroups = blockDim.x / MPNL_GROUP;
-  const TravSmem so(a.m, N, a.vc, tp.list_bytes, ngroups);
+  const int nth = blockDim.x, nw = nth >> 5;
+  const TravSmem so(a.m, N, nw);
   const TableLayout tl(a.m, N);
   const int m = a.m;
   const int64_t c = blockIdx.x / a.chunks;
   const int v0 = (blockIdx.x % a.chunks) * a.vc;
   const int vce = (int)min((int64_t)a.vc, a.V - v0);
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int P = tp.n_paths;
-
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const float INF = __int_as_float(0x7f800000);
+  TreeParams& tp = *reinterpret_cast<TreeParams*>(sm + so.tpo);
   float* tab = sm + so.tab;
-  float2* ys = reinterpret_cast<float2*>(sm + so.y);
-  float2* zs = reinterpret_cast<float2*>(sm + so.z);
-  float* thr = sm + so.thr;
-  float* vb1 = sm + so.vb1;
-  float* vb2 = sm + so.vb2;
-  float* vfm = sm + so.vfm;
-  int* vbp = reinterpret_cast<int*>(sm + so.vbp);
-  float* vcorr = sm + so.vcorr;
-  float* misc = sm + so.misc;
-  uint8_t* lists = reinterpret_cast<uint8_t*>(sm) + so.lists;
-
-  // ---------------- phase A: stage + rotate ----------------
+  float2* zs = reinterpret_cast<float2*>(sm + so.wz) + warp * MPNL_VPI_MAX * N;
+  float* thr = sm + so.wthr + warp * MPNL_VPI_MAX * N;
+  float2* ys = reinterpret_cast<float2*>(sm + so.wy) + warp * MPNL_MAX_M;
+  int4* evb = reinterpret_cast<int4*>(sm + so.ev);
+  int* evn = reinterpret_cast<int*>(sm + so.evn);
   {
+    const int* s = reinterpret_cast<const int*>(&tparam);
+    int* d = reinterpret_cast<int*>(&tp);
+    for (int i = tid; i < (int)(sizeof(TreeParams) / 4); i += nth) d[i] = s[i];
     const float4* src = reinterpret_cast<const float4*>(a.tables + c * (int64_t)tl.total);
     float4* dst = reinterpret_cast<float4*>(tab);
     for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
-    const int64_t ybase = (c * a.V + v0) * (int64_t)m;
-    if (a.y_f64) {
-      const double2* yd = reinterpret_cast<const double2*>(a.y) + ybase;
-      for (int i = tid; i < vce * m; i += nth) {
-        const double2 v = yd[i];
-        ys[i] = make_float2((float)v.x, (float)v.y);
-      }
-    } else {
-      const float2* yf = reinterpret_cast<const float2*>(a.y) + ybase;
-      for (int i = tid; i < vce * m; i += nth) ys[i] = yf[i];
-    }
-    for (int i = tid; i < a.vc; i += nth) {
-      vfm[i] = __int_as_float(0x7f800000);
-      vcorr[i] = 0.f;
-    }
-    if (tid == 0) { misc[0] = 0.f; misc[1] = 0.f; }
+    if (tid == 0) { evn[0] = 0; evn[1] = 0; }
   }
   __syncthreads();
-  {
-    const float2* qh = reinterpret_cast<const float2*>(tab + tl.off_qh);
-    const float2* sh = reinterpret_cast<const float2*>(tab + tl.off_shift);
-    for (int i = tid; i < vce * N; i += nth) {
-      const int v = i / N, k = i - v * N;
-      float zr = 0.f, zi = 0.f;
-      for (int r = 0; r < m; ++r) {
-        const float2 q = qh[k * m + r], yv = ys[v * m + r];
-        zr = __fmaf_rn(q.x, yv.x, zr);
-        zr = __fmaf_rn(-q.y, yv.y, zr);
-        zi = __fmaf_rn(q.x, yv.y, zi);
-        zi = __fmaf_rn(q.y, yv.x, zi);
-      }
-      zs[i] = make_float2(__fsub_rn(zr, sh[k].x), __fsub_rn(zi, sh[k].y));
-    }
-    for (int v = tid; v < vce; v += nth) {
-      float yn = 0.f;
-      for (int r = 0; r < m; ++r) {
-        const float2 yv = ys[v * m + r];
-        yn = __fmaf_rn(yv.x, yv.x, __fmaf_rn(yv.y, yv.y, yn));
-      }
-      if (a.metric_offset) vcorr[v] = yn;
-      atomicMax(reinterpret_cast<int*>(misc), __float_as_int(sqrtf(yn)));
-    }
-  }
-  __syncthreads();
-  {
-    const float4* lay4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
-    const float ymax = misc[0];
-    float eacc = 0.f;
-    for (int k = tid; k < N; k += nth) {
-      const float4 ly = lay4[k];
-      const float ek = a.tau * (ymax + ly.z);          // acc-domain error bound
-      thr[k] = 0.5f - ek / ly.y;                        // index-domain threshold
-      eacc = fmaxf(eacc, ek);
-    }
-    if (tid < N) atomicMax(reinterpret_cast<int*>(misc + 1), __float_as_int(eacc));
-    if (a.metric_offset) {
-      const float2* sh = reinterpret_cast<const float2*>(tab + tl.off_shift);
-      for (int v = tid; v < vce; v += nth) {
-        float zn = 0.f;
-        for (int k = 0; k < N; ++k) {
-          const float2 z = zs[v * N + k];
-          const float zr = z.x + sh[k].x, zi = z.y + sh[k].y;
-          zn = __fmaf_rn(zr, zr, __fmaf_rn(zi, zi, zn));
-        }
-        vcorr[v] = vcorr[v] - zn;
-      }
-    }
-  }
-  __syncthreads();
+  const TabPtrs T = tab_ptrs(tab, m, N);
+  const int P = tp.n_paths;
+  const bool batch = a.bpv > 1 || a.vpi == 1;
+  const int nvi = batch ? 1 : a.vpi;                       // vectors per item
+  const int items = (vce + nvi - 1) / nvi;
+  const int64_t gbase = c * a.V + v0;
 
-  // ---------------- phase B: partial-layer selection lists ----------------
-  if (a.has_partial) {
-    constexpr int NP = (N + 1) & ~1;
-    const float* rcol = tab + tl.off_rcol;
-    const float4* lay4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
-    const int gid = tid / MPNL_GROUP, gl = tid % MPNL_GROUP;
-    float* gs = sm + so.gscr + gid * MPNL_GSCR;   // dx[8] dy[8] key[64] ox/oy(4) de de1
-    float* gdx = gs;
-    float* gdy = gs + 8;
-    float* gkey = gs + 16;
-    uint8_t* gox = reinterpret_cast<uint8_t*>(gs + 80);
-    uint8_t* goy = gox + 8;
-    const int top_lo = N - tp.n_top;
-    for (int pos = N - 1; pos >= top_lo; --pos) {
-      const int e = tp.e[pos];
-      if (e == L * L) continue;
-      const int npar = P / tp.stride[pos + 1];
-      const int K = tp.stair_cnt[pos];
-      const int items = vce * npar;
-      const float4 lyp = lay4[pos];
-      for (int it0 = 0; it0 < items; it0 += ngroups) {
-        const int it = it0 + gid;
-        const bool act = it < items;
-        const int vl = act ? it / npar : 0;
-        const int par = act ? it - vl * npar : 0;
-        const int p0 = par * tp.stride[pos + 1];
-        const uint8_t* vlist = lists + vl * tp.list_bytes;
-        // prefix: acc at every prefix layer (phase-C order), PED prefix, acc at pos
-        float pedp = 0.f, xr = 0.f, xi = 0.f;
-        for (int j = N - 1; j >= pos; --j) {
-          const float2 zj = zs[vl * N + j];
-          float ar_ = zj.x, ai_ = zj.y;
-          for (int l = N - 1; l > j; --l) {
-            int ir, ii;
-            expanded_symbol<L>(tp, l, p0, vlist, ir, ii);
-            const float fr = (float)ir, fi = (float)ii;
-            const float2 r2 = reinterpret_cast<const float2*>(rcol + 2 * NP * l)[j];
-            ar_ = __fmaf_rn(r2.x, fr, ar_);
-            ar_ = __fmaf_rn(-r2.y, fi, ar_);
-            ai_ = __fmaf_rn(r2.x, fi, ai_);
-            ai_ = __fmaf_rn(r2.y, fr, ai_);
-          }
-          if (j > pos) {
-            int ir, ii;
-            expanded_symbol<L>(tp, j, p0, vlist, ir, ii);
-            const float c2r = lay4[j].y;
-            const float er = __fmaf_rn(c2r, (float)ir, ar_);
-            const float ei = __fmaf_rn(c2r, (float)ii, ai_);
-            pedp = __fmaf_rn(er, er, pedp);
-            pedp = __fmaf_rn(ei, ei, pedp);
-          } else {
-            xr = ar_; xi = ai_;
-          }
-        }
-        // centre in level-index units (unclamped)
-        const float cx = __fmul_rn(__fmul_rn(xr, lyp.x), (float)(L - 1));
-        const float cy = __fmul_rn(__fmul_rn(xi, lyp.x), (float)(L - 1));
-        if (gl == 0 && act) {
-          // per-axis Schnorr-Euchner (closest-first) level orders
+  for (int item = warp; item < items; item += nw) {
+    // ---- prologue per vector: z' (lane = row), per-layer bounds, E_acc ----
+    float eacc_v[MPNL_VPI_MAX];
 #pragma unroll
-          for (int ax = 0; ax < 2; ++ax) {
-            const float x = ax ? cy : cx;
-            float* dd = ax ? gdy : gdx;
-            uint8_t* oo = ax ? goy : gox;
-            const int n0 = (int)rintf(fminf(fmaxf(x, 0.f), (float)(L - 1)));
-            int lo = n0 - 1, hi = n0 + 1;
-            oo[0] = (uint8_t)n0;
-            dd[0] = (x - n0) * (x - n0);
-#pragma unroll
-            for (int r = 1; r < L; ++r) {
-              const bool th = (hi < L) && (lo < 0 || (hi - x) < (x - lo));
-              const int lev = th ? hi : lo;
-              if (th) ++hi; else --lo;
-              oo[r] = (uint8_t)lev;
-              dd[r] = (x - lev) * (x - lev);
-            }
-          }
-        }
-        __syncwarp();
-        // staircase(e+1) candidates (i, j) with (i+1)(j+1) <= e+1
-        for (int cc = gl; cc < K; cc += MPNL_GROUP) {
-          int i = 0, rem = cc;
-          while (true) {
-            const int w = min(L, (e + 1) / (i + 1));
-            if (rem < w) break;
-            rem -= w;
-            ++i;
-          }
-          if (act) gkey[cc] = gdx[i] + gdy[rem];
-        }
-        __syncwarp();
-        for (int cc = gl; cc < K; cc += MPNL_GROUP) {
-          int i = 0, rem = cc;
-          while (true) {
-            const int w = min(L, (e + 1) / (i + 1));
-            if (rem < w) break;
-            rem -= w;
-            ++i;
-          }
-          if (!act) continue;
-          const float key = gkey[cc];
-          int rank = 0;
-          for (int c2 = 0; c2 < K; ++c2) {
-            const float k2 = gkey[c2];
-            rank += (k2 < key) || (k2 == key && c2 < cc);
-          }
-          if (rank < e) lists[vl * tp.list_bytes + tp.list_off[pos] + par * e + rank] =
-                            (uint8_t)((gox[i] << 3) | goy[rem]);
-          if (rank == e - 1) gs[84] = key;
-          if (rank == e) gs[85] = key;
-        }
-        __syncwarp();
-        if (gl == 0 && act) {
-          const float E = fmaxf(0.5f - thr[pos], 0.f);
-          const float de = gs[84], de1 = gs[85];
-          const float bound = 2.8284272f * E * (sqrtf(de) + sqrtf(de1)) + 4.f * E * E +
-                              4.8e-7f * de1;
-          if (de1 - de <= bound)
-            atomicMin(reinterpret_cast<int*>(vfm + vl), __float_as_int(pedp));
-        }
-        __syncwarp();
+    for (int j = 0; j < MPNL_VPI_MAX; ++j) {
+      eacc_v[j] = 0.f;
+      const int vl = item * nvi + j;
+      if (j >= nvi || vl >= vce) continue;
+      const int64_t gv = gbase + vl;
+      float yp = 0.f;
+      for (int r = lane; r < m; r += 32) {
+        const float2 v = load_y32(a, gv * m + r);
+        ys[r] = v;
+        yp = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, yp));
       }
-      __syncthreads();
+      const float ynorm = sqrtf(warp_sum(yp)) * 1.0001f;
+      __syncwarp();
+      float e2 = 0.f;
+      if (lane < N) {
+        const float2 z = rotate_row(tab, m, N, lane, [&](int r) { return ys[r]; });
+        zs[j * N + lane] = z;
+        a.zq[gv * N + lane] = z;
+        const float4 ly = T.lay4[lane];
+        const float e = row_bound(ynorm, z, ly, lane, m, N, L, a.guard_scale);
+        thr[j * N + lane] = 0.5f - e / ly.y - MPNL_U * 2.f * L;
+        e2 = e * e;
+      }
+      eacc_v[j] = sqrtf(warp_sum(e2)) * 1.001f;
+      __syncwarp();
     }
-  }
 
-  // ---------------- phase C: path traversal + warp argmin ----------------
-  {
-    const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
-    const int items = (a.bpv > 1 || a.vpi == 1) ? (a.bpv > 1 ? vce : (vce + a.vpi - 1) / a.vpi)
-                                                : (vce + a.vpi - 1) / a.vpi;
-    int dummy_lab[N];
-    for (int item = warp; item < items; item += nw) {
-      Best run = {__int_as_float(0x7f800000), __int_as_float(0x7f800000),
-                  __int_as_float(0x7f800000), 0x7fffffff};
-      for (int b = 0; b < a.bpv; ++b) {
-        int vl[PT], pp[PT];
-        bool ok[PT];
+    // ---- traversal over path batches ----
+    Top3 run = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
+    float wb = INF;   // warp-wide best so far of this vector (batch mode)
+    for (int b = 0; b < a.bpv; ++b) {
+      int vl[PT], pp[PT];
+      int64_t gvl[PT];
+      bool ok[PT];
+#pragma unroll
+      for (int t = 0; t < PT; ++t) {
+        const int s = t * 32 + lane;
+        if (batch) {
+          vl[t] = 0;
+          pp[t] = b * S + s;
+          ok[t] = pp[t] < P;
+        } else {
+          vl[t] = s / P;
+          pp[t] = s % P;
+          ok[t] = vl[t] < nvi && item * nvi + vl[t] < vce;
+        }
+        if (!ok[t]) { vl[t] = 0; pp[t] = 0; }
+        gvl[t] = gbase + item * nvi + vl[t];
+      }
+      float ped[PT], evp[PT];
+      unsigned evm[PT];
+      traverse_paths<N, L, PT>(T, zs, thr, a.lists, tp, tp.list_bytes, vl, gvl, pp, ped, evm, evp);
+      // log paths with a marked decision whose prefix may still be competitive
+      const float bnd = (wb == INF) ? INF : wb + 2.f * ped_tol(wb, eacc_v[0], N);
+#pragma unroll
+      for (int t = 0; t < PT; ++t) {
+        if (ok[t] && evm[t] != 0u && evp[t] <= bnd) {
+          const int4 e4 = make_int4(pp[t], (int)evm[t], (int)gvl[t], EV_NODE);
+          const int idx = atomicAdd(evn, 1);
+          if (idx < TRAV_EV_CAP) evb[idx] = e4;
+          else log_event(a, e4);
+        }
+      }
+      if (batch) {
+#pragma unroll
+        for (int t = 0; t < PT; ++t)
+          if (ok[t]) top3_insert(run, ped[t], (unsigned)pp[t]);
+        wb = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
+      } else if (P >= 32) {
+        const int g = P >> 5;   // t-slots per vector
+#pragma unroll
+        for (int t0 = 0; t0 < PT; ++t0) {
+          if (t0 % g) continue;
+          Top3 x = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
+#pragma unroll
+          for (int t = 0; t < PT; ++t)
+            if (t >= t0 && t < t0 + g && ok[t]) top3_insert(x, ped[t], (unsigned)pp[t]);
+          float b1, b2, b3;
+          unsigned q1, q2;
+          warp_top3(x, b1, q1, b2, q2, b3);
+          const int j = t0 / g;
+          const int vlj = item * nvi + j;
+          if (lane == 0 && j < nvi && vlj < vce) {
+            float ej = 0.f;
+#pragma unroll
+            for (int jj = 0; jj < MPNL_VPI_MAX; ++jj)
+              if (jj == j) ej = eacc_v[jj];
+            a.vres[gbase + vlj] = make_float4(b1, b2, b3, ej);
+            a.vpath[gbase + vlj] = make_int2((int)q1, (int)q2);
+          }
+        }
+      } else {
 #pragma unroll
         for (int t = 0; t < PT; ++t) {
-          const int s = t * 32 + lane;
-          if (a.bpv > 1 || a.vpi == 1) {
-            vl[t] = item;
-            pp[t] = b * S + s;
-            ok[t] = pp[t] < P;
-          } else {
-            vl[t] = item * a.vpi + s / P;
-            pp[t] = s % P;
-            ok[t] = vl[t] < vce;
+          Top3 x = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
+          if (ok[t]) top3_insert(x, ped[t], (unsigned)pp[t]);
+          float b1, b2, b3;
+          unsigned q1, q2;
+          group_top3(x, P, b1, q1, b2, q2, b3);
+          const int j = (t * 32 + lane) / P;
+          const int vlj = item * nvi + j;
+          if ((lane % P) == 0 && j < nvi && vlj < vce) {
+            float ej = 0.f;
+#pragma unroll
+            for (int jj = 0; jj < MPNL_VPI_MAX; ++jj)
+              if (jj == j) ej = eacc_v[jj];
+            a.vres[gbase + vlj] = make_float4(b1, b2, b3, ej);
+            a.vpath[gbase + vlj] = make_int2((int)q1, (int)q2);
           }
-          if (!ok[t]) { vl[t] = 0; pp[t] = 0; }
-        }
-        float ped[PT], fped[PT];
-        traverse_paths<N, L, PT, true, false>(tab, zs, thr, lists, tp, tp.list_bytes, vl, pp,
-                                              ped, fped, dummy_lab, m);
-        if (a.bpv > 1 || a.vpi == 1) {
-#pragma unroll
-          for (int t = 0; t < PT; ++t) {
-            Best x = {ok[t] ? ped[t] : __int_as_float(0x7f800000), __int_as_float(0x7f800000),
-                      ok[t] ? fped[t] : __int_as_float(0x7f800000), ok[t] ? pp[t] : 0x7fffffff};
-            run = best_merge(run, x);
-          }
-        } else if (P >= 32) {
-          const int g = P >> 5;   // t-slots per vector
-#pragma unroll
-          for (int t0 = 0; t0 < PT; ++t0) {
-            if (t0 % g) continue;
-            Best x = {__int_as_float(0x7f800000), __int_as_float(0x7f800000),
-                      __int_as_float(0x7f800000), 0x7fffffff};
-#pragma unroll
-            for (int t = 0; t < PT; ++t)
-              if (t >= t0 && t < t0 + g) {
-                Best y = {ok[t] ? ped[t] : __int_as_float(0x7f800000),
-                          __int_as_float(0x7f800000),
-                          ok[t] ? fped[t] : __int_as_float(0x7f800000), pp[t]};
-                x = best_merge(x, y);
-              }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) x = best_shfl(x, o);
-            const int v = item * a.vpi + t0 / g;
-            if (lane == 0 && v < vce) {
-              vb1[v] = x.b1; vb2[v] = x.b2; vbp[v] = x.bp; vfm[v] = fminf(vfm[v], x.fm);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int t = 0; t < PT; ++t) {
-            Best x = {ok[t] ? ped[t] : __int_as_float(0x7f800000), __int_as_float(0x7f800000),
-                      ok[t] ? fped[t] : __int_as_float(0x7f800000), pp[t]};
-            for (int o = P >> 1; o; o >>= 1) x = best_shfl(x, o);
-            const int v = item * a.vpi + (t * 32 + lane) / P;
-            if ((lane % P) == 0 && v < vce) {
-              vb1[v] = x.b1; vb2[v] = x.b2; vbp[v] = x.bp; vfm[v] = fminf(vfm[v], x.fm);
-            }
-          }
-        }
-      }
-      if (a.bpv > 1 || a.vpi == 1) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) run = best_shfl(run, o);
-        if (lane == 0) {
-          vb1[item] = run.b1; vb2[item] = run.b2; vbp[item] = run.bp;
-          vfm[item] = fminf(vfm[item], run.fm);
         }
       }
     }
+    if (batch) {
+      float b1, b2, b3;
+      unsigned q1, q2;
+      warp_top3(run, b1, q1, b2, q2, b3);
+      if (lane == 0) {
+        a.vres[gbase + item] = make_float4(b1, b2, b3, eacc_v[0]);
+        a.vpath[gbase + item] = make_int2((int)q1, (int)q2);
+      }
+    }
+  }
+  // ---- flush the CTA's event buffer to the global log ----
+  __syncthreads();
+  const int n_ev = min(evn[0], TRAV_EV_CAP);
+  if (tid == 0) evn[1] = n_ev ? atomicAdd(a.counters + 1, n_ev) : 0;
+  __syncthreads();
+  const int base = evn[1];
+  for (int i = tid; i < n_ev; i += nth) {
+    if (base + i < a.ev_cap) a.events[base + i] = evb[i];
+    else send_to_fp64(a, (int64_t)(unsigned)evb[i].z);
+  }
+}
+
+// ===========================================================================
+// K4: verification — winners (thread per vector) and events (thread per event)
+// ===========================================================================
+template <int N, int L>
+__global__ void __launch_bounds__(128)
+verify_kernel(const DetectArgs a, const TreeParams tparam, int vec_blocks) {
+  __shared__ TreeParams tp;
+  {
+    const int* s = reinterpret_cast<const int*>(&tparam);
+    int* d = reinterpret_cast<int*>(&tp);
+    for (int i = threadIdx.x; i < (int)(sizeof(TreeParams) / 4); i += blockDim.x) d[i] = s[i];
   }
   __syncthreads();
-
-  // ---------------- phase D: re-trace winners, labels, guard verdict ----------------
-  {
-    const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
-    const float eacc = misc[1];
-    const int32_t* pc = a.perm + c * N;
-    for (int v = tid; v < vce; v += nth) {
-      int vl[1] = {v}, pp[1] = {vbp[v]};
-      float ped[1], fped[1];
-      int lab[N];
-      traverse_paths<N, L, 1, false, true>(tab, zs, thr, lists, tp, tp.list_bytes, vl, pp, ped,
-                                           fped, lab, m);
-      const int64_t gv = c * a.V + v0 + v;
-      uint8_t* out = a.hard + gv * N;
+  const int m = a.m;
+  const TableLayout tl(m, N);
+  const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
+  const int64_t B = a.n_ch * a.V;
+  float2 zl[N];
+  int lab[N];
+  float pre[N];
+  auto prep = [&](int64_t gv, const float*& tab) {
+    const int64_t c = gv / a.V;
+    tab = a.tables + c * (int64_t)tl.total;
 #pragma unroll
-      for (int pos = 0; pos < N; ++pos) {
-        const int ir = lab[pos] >> 3, ii = lab[pos] & 7;
-        out[pc[pos]] = (uint8_t)((gray_code(ir) << h) | gray_code(ii));
+    for (int k = 0; k < N; ++k) zl[k] = a.zq[gv * N + k];
+    return c;
+  };
+  if ((int)blockIdx.x < vec_blocks) {
+    const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gv >= B) return;
+    const float* tab;
+    const int64_t c = prep(gv, tab);
+    const uint8_t* vlist = a.lists + gv * tp.list_bytes;
+    const float4 res = a.vres[gv];
+    const int2 pth = a.vpath[gv];
+    retrace_inline<N, L>(tab, m, zl, vlist, tp, pth.x, 0, lab, pre);
+    float met = res.x;
+    if (res.y - res.x <= ped_tol(res.x, res.w, N) + ped_tol(res.y, res.w, N)) {
+      // near-tie of the two best paths: decide between them in fp64
+      if (res.z - res.x <= ped_tol(res.x, res.w, N) + ped_tol(res.z, res.w, N)) {
+        send_to_fp64(a, gv);                  // three-way: full fp64 recompute
+      } else {
+        if (a.stats) atomicAdd(a.stats + 2, 1);
+        int lab2[N];
+        retrace_path<N, L>(tab, m, zl, vlist, tp, pth.y, 0, lab2, pre);
+        const double m1 = ped_f64(a, c, gv, N, lab, L), m2 = ped_f64(a, c, gv, N, lab2, L);
+        if (fabs(m1 - m2) <= 1e-12 * fmax(m1, m2)) {
+          send_to_fp64(a, gv);                // tie at fp64 level: exact total order
+        } else if (m2 < m1) {
+#pragma unroll
+          for (int k = 0; k < N; ++k) lab[k] = lab2[k];
+          met = res.y;
+        }
       }
-      const float b1 = vb1[v], b2 = vb2[v], fm = vfm[v];
-      a.metric[gv] = b1 + vcorr[v];
-      const float tolm = 4.f * sqrtf((float)N * b1) * eacc + 2.f * N * eacc * eacc + 2e-6f * b1;
-      const bool flag = (b2 - b1 <= 2e-5f * b1 + tolm) || (fm <= b1 + tolm);
-      if (a.flags) a.flags[gv] = flag ? 1 : 0;
-      if (flag) {
-        const int slot = atomicAdd(a.flag_count, 1);
-        a.flag_list[slot] = gv;
+    }
+    float corr = 0.f;
+    if (a.metric_offset) {
+      const float2* sh = reinterpret_cast<const float2*>(tab + tl.off_shift);
+      float yn = 0.f, zn = 0.f;
+      for (int r = 0; r < m; ++r) {
+        const float2 v = load_y32(a, gv * m + r);
+        yn = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, yn));
       }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const float zr = zl[k].x + sh[k].x, zi = zl[k].y + sh[k].y;
+        zn = __fmaf_rn(zr, zr, __fmaf_rn(zi, zi, zn));
+      }
+      corr = yn - zn;
+    }
+    const int32_t* pc = a.perm + c * N;
+    uint8_t* out = a.hard + gv * N;
+#pragma unroll
+    for (int pos = 0; pos < N; ++pos) {
+      const int ir = lab[pos] >> 3, ii = lab[pos] & 7;
+      out[pc[pos]] = (uint8_t)((gray_code(ir) << h) | gray_code(ii));
+    }
+    a.metric[gv] = met + corr;
+    return;
+  }
+  // ---- events ----
+  const int nev = min(a.counters[1], a.ev_cap);
+  const double nrm = qam_norm_d(L);
+  const int stride = (gridDim.x - vec_blocks) * blockDim.x;
+  for (int i = (blockIdx.x - vec_blocks) * blockDim.x + threadIdx.x; i < nev; i += stride) {
+    const int4 e4 = a.events[i];
+    const int64_t gv = (int64_t)(unsigned)e4.z;
+    if (a.vflag[gv]) continue;
+    const float4 res = a.vres[gv];
+    const float lim = res.x + 2.f * ped_tol(res.x, res.w, N);
+    const float* tab;
+    const int64_t c = prep(gv, tab);
+    const uint8_t* vlist = a.lists + gv * tp.list_bytes;
+    if (e4.w == EV_NODE) {
+      const unsigned mask = (unsigned)e4.y;
+      const int lowest = __ffs(mask) - 1;
+      retrace_path<N, L>(tab, m, zl, vlist, tp, e4.x, lowest, lab, pre);
+      for (int pos = N - 1; pos >= lowest; --pos) {
+        if (!((mask >> pos) & 1u) || pre[pos] > lim) continue;
+        if (a.stats) atomicAdd(a.stats + 1, 1);
+        double cr, ci;
+        centre_f64(a, c, gv, N, pos, lab, L, cr, ci);
+        const int ir = nearest_level_f64(cr, L, nrm), ii = nearest_level_f64(ci, L, nrm);
+        if (ir * 8 + ii != lab[pos]) { send_to_fp64(a, gv); break; }
+      }
+    } else {
+      const int pos = e4.y;
+      if (pos < N - 1) retrace_path<N, L>(tab, m, zl, vlist, tp, e4.x, pos + 1, lab, pre);
+      const float prefix = (pos < N - 1) ? pre[pos + 1] : 0.f;   // <= PED prefix at pos
+      if (prefix > lim) continue;
+      if (a.stats) atomicAdd(a.stats + 1, 1);
+      double cr, ci;
+      centre_f64(a, c, gv, N, pos, lab, L, cr, ci);
+      const int e = tp.e[pos];
+      const unsigned long long m64 = nearest_set_f64(cr, ci, L, nrm, e);
+      const int par = e4.x / tp.stride[pos + 1];
+      const uint8_t* lst = vlist + tp.list_off[pos] + par * e;
+      unsigned long long m32 = 0ull;
+      for (int r = 0; r < e; ++r) m32 |= 1ull << ((lst[r] >> 3) * L + (lst[r] & 7));
+      if (m32 != m64) send_to_fp64(a, gv);
     }
   }
 }

@@ -1,33 +1,37 @@
-// Explicit instantiation of the traversal kernel for one QAM order (L levels
-// per axis) and a range of N, plus the launcher the C ABI dispatches to.
-// Included by the generated traverse_l<L>_p<part>.cu units (one per
-// constellation x N-range of 8, compiled in parallel).
+// Explicit instantiation of the fast-path kernels (select / traverse / verify)
+// for one QAM order (L levels per axis) and a range of 8 N values, plus the
+// launcher the C ABI dispatches to.  Included by the traverse_l<L>_p<part>.cu
+// units (one per constellation x N-range, compiled in parallel).
 #pragma once
 #include "traverse.cuh"
 
 namespace mpnl {
 
+// kind 0 = select_kernel (extra = layer), 1 = traverse_kernel, 2 = verify_kernel
+// (extra = number of per-vector blocks)
 template <int NN, int L>
-cudaError_t launch_traverse_one(const TraverseArgs& a, const TreeParams& tp, int threads,
-                                unsigned grid, size_t smem, cudaStream_t st) {
-  auto k = traverse_kernel<NN, L>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<grid, threads, smem, st>>>(a, tp);
+cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp, unsigned grid,
+                            int threads, size_t smem, int extra, cudaStream_t st) {
+  if (kind == 0) {
+    select_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
+  } else if (kind == 1) {
+    auto k = traverse_kernel<NN, L>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, threads, smem, st>>>(a, tp);
+  } else {
+    verify_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
+  }
   return cudaGetLastError();
 }
 
 template <int L, int N0>
-cudaError_t launch_traverse_part(int n, const TraverseArgs& a, const TreeParams& tp, int threads,
-                                 unsigned grid, size_t smem, cudaStream_t st) {
+cudaError_t launch_fast_part(int n, int kind, const DetectArgs& a, const TreeParams& tp,
+                             unsigned grid, int threads, size_t smem, int extra, cudaStream_t st) {
   switch (n - N0) {
-    case 0: return launch_traverse_one<N0 + 0, L>(a, tp, threads, grid, smem, st);
-    case 1: return launch_traverse_one<N0 + 1, L>(a, tp, threads, grid, smem, st);
-    case 2: return launch_traverse_one<N0 + 2, L>(a, tp, threads, grid, smem, st);
-    case 3: return launch_traverse_one<N0 + 3, L>(a, tp, threads, grid, smem, st);
-    case 4: return launch_traverse_one<N0 + 4, L>(a, tp, threads, grid, smem, st);
-    case 5: return launch_traverse_one<N0 + 5, L>(a, tp, threads, grid, smem, st);
-    case 6: return launch_traverse_one<N0 + 6, L>(a, tp, threads, grid, smem, st);
-    case 7: return launch_traverse_one<N0 + 7, L>(a, tp, threads, grid, smem, st);
+#define MPNL_C(I) \
+    case I: return launch_fast_one<N0 + I, L>(kind, a, tp, grid, threads, smem, extra, st);
+    MPNL_C(0) MPNL_C(1) MPNL_C(2) MPNL_C(3) MPNL_C(4) MPNL_C(5) MPNL_C(6) MPNL_C(7)
+#undef MPNL_C
     default: return cudaErrorInvalidValue;
   }
 }

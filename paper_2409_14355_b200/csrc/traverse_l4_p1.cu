@@ -1,9 +1,10 @@
-// Generated: traversal kernels for 16-QAM, N = 9..16.
+// Generated: fast-path kernels for 16-QAM, N = 9..16.
 #include "traverse_inst.cuh"
 
 namespace mpnl {
-cudaError_t launch_traverse_l4_p1(int n, const TraverseArgs& a, const TreeParams& tp,
-                                        int threads, unsigned grid, size_t smem, cudaStream_t st) {
-  return launch_traverse_part<4, 9>(n, a, tp, threads, grid, smem, st);
+cudaError_t launch_fast_l4_p1(int n, int kind, const DetectArgs& a, const TreeParams& tp,
+                                    unsigned grid, int threads, size_t smem, int extra,
+                                    cudaStream_t st) {
+  return launch_fast_part<4, 9>(n, kind, a, tp, grid, threads, smem, extra, st);
 }
 }  // namespace mpnl

@@ -241,7 +241,8 @@ def mpnl_detect_hard(plan: BatchPathPlan, h, y, c: Constellation, *, return_flag
     hard = torch.empty((nch, v, n), dtype=torch.uint8, device=dev)
     metric = torch.empty((nch, v), dtype=torch.float32, device=dev)
     flags = torch.empty((nch, v), dtype=torch.uint8, device=dev) if return_flags else None
-    ws = torch.empty(int(lib.mpnl_workspace_bytes(nch * v)), dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(lib.mpnl_workspace_bytes(nch * v, n, c.order, plan.expansions.ctypes.data)),
+                     dtype=torch.uint8, device=dev)
     rc = lib.mpnl_detect_hard(plan.perm_dev.data_ptr(), plan.r_dev.data_ptr(),
                               plan.qh_dev.data_ptr(), plan.tables.data_ptr(), yd.data_ptr(),
                               int(y64), nch, v, m, n, c.order, plan.expansions.ctypes.data,

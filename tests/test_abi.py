@@ -65,4 +65,5 @@ def test_shim_allocate_expansions_warns():
 def test_tables_and_workspace_sizes():
     lib = _lib.load()
     assert lib.mpnl_tables_floats(12, 12) % 4 == 0
-    assert lib.mpnl_workspace_bytes(1000) >= 16 + 8 * 1000
+    ex = np.array([1] * 10 + [4, 16], dtype=np.int64)
+    assert lib.mpnl_workspace_bytes(1000, 12, 16, ex.ctypes.data) >= 1000 * (8 + 4 + 16 + 8 + 64)
