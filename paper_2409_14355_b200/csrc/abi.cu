@@ -330,12 +330,14 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     // the per-CTA table staging is a few KB)
     const int unit = (bpv > 1 || vpi == 1 ? 1 : vpi) * warps;
     int64_t vc = std::min<int64_t>(4 * unit, v_per_ch);
+    while (vc > unit && TravSmem(m, n, warps, (int)vc, tp.list_bytes).total_bytes > 56 * 1024)
+      vc -= unit;
     const int64_t chunks = (v_per_ch + vc - 1) / vc;
     if (n_ch * chunks > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
     a.vc = (int)vc;
     a.chunks = (int)chunks;
     if (stage == 2) {
-      const TravSmem so(m, n, warps);
+      const TravSmem so(m, n, warps, (int)vc, tp.list_bytes);
       e = launch_fast(n, L, 1, a, tp, (unsigned)(n_ch * chunks), threads, so.total_bytes, 0, st);
       if (e != cudaSuccess) return cuda_fail(e, "traverse kernel");
     } else {

@@ -302,11 +302,24 @@ static __device__ __noinline__ void retrace_path(const float* tab, int m, const 
   retrace_inline<N, L>(tab, m, zs, vlist, tp, p, stop, lab, pre);
 }
 
+// Paths per lane: more paths amortise the r'' loads and add ILP, but the
+// fully unrolled traversal grows as PT * N^2 instructions; beyond N = 16 the
+// two-path loop no longer fits the instruction cache (ncu: no_instruction
+// stalls dominate), so large N runs one path per lane at twice the warps.
+#ifndef MPNL_PT_SMALL
+#define MPNL_PT_SMALL 4
+#endif
+#ifndef MPNL_PT_MID
+#define MPNL_PT_MID 2
+#endif
+#ifndef MPNL_PT_LARGE
+#define MPNL_PT_LARGE 1
+#endif
 template <int N>
 struct TravCfg {
-  static constexpr int PT = N <= 8 ? 4 : 2;              // paths per lane
+  static constexpr int PT = N <= 8 ? MPNL_PT_SMALL : (N <= 16 ? MPNL_PT_MID : MPNL_PT_LARGE);
   static constexpr int MAXT = 128;                       // threads per CTA
-  static constexpr int MINB = N <= 16 ? 4 : 2;           // CTAs per SM
+  static constexpr int MINB = PT * N <= 48 ? 4 : (PT * N <= 64 ? 3 : 2);   // CTAs per SM
 };
 
 // ---------------------------------------------------------------------------
@@ -588,18 +601,20 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
 // K3: traversal (hot kernel)
 // ===========================================================================
 struct TravSmem {
-  int tpo, tab, wz, wthr, wy, ev, evn, total_bytes;
-  __host__ __device__ TravSmem(int m, int n, int warps) {
+  int tpo, tab, wz, wthr, wy, ev, evn, ylist, lists, total_bytes;
+  __host__ __device__ TravSmem(int m, int n, int warps, int vc, int list_bytes) {
     TableLayout tl(m, n);
     int o = 0;
     tpo = o; o += TableLayout::up4((int)(sizeof(TreeParams) / 4));
     tab = o; o += tl.total;
     wz = o; o += warps * 2 * MPNL_VPI_MAX * n;     // per warp z' (VPI x N float2)
     wthr = o; o += warps * MPNL_VPI_MAX * n;       // per warp thresholds
-    wy = o; o += warps * 2 * MPNL_MAX_M;           // per warp y (float2)
+    wy = o; o += 0;                                // (unused)
     ev = o; o += 4 * TRAV_EV_CAP;                  // int4 event buffer
     evn = o; o += 4;
-    total_bytes = o * 4;
+    ylist = o; o += TableLayout::up4(2 * vc * m); // the chunk's y (fp32)
+    lists = o * 4;                                 // the chunk's selection lists (bytes)
+    total_bytes = lists + ((vc * list_bytes + 15) & ~15);
   }
 };
 
@@ -610,7 +625,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   constexpr int S = 32 * PT;
   extern __shared__ __align__(16) float sm[];
   const int nth = blockDim.x, nw = nth >> 5;
-  const TravSmem so(a.m, N, nw);
+  const TravSmem so(a.m, N, nw, a.vc, tparam.list_bytes);
   const TableLayout tl(a.m, N);
   const int m = a.m;
   const int64_t c = blockIdx.x / a.chunks;
@@ -622,7 +637,8 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   float* tab = sm + so.tab;
   float2* zs = reinterpret_cast<float2*>(sm + so.wz) + warp * MPNL_VPI_MAX * N;
   float* thr = sm + so.wthr + warp * MPNL_VPI_MAX * N;
-  float2* ys = reinterpret_cast<float2*>(sm + so.wy) + warp * MPNL_MAX_M;
+  float2* ych = reinterpret_cast<float2*>(sm + so.ylist);
+  uint8_t* lch = reinterpret_cast<uint8_t*>(sm) + so.lists;
   int4* evb = reinterpret_cast<int4*>(sm + so.ev);
   int* evn = reinterpret_cast<int*>(sm + so.evn);
   {
@@ -633,6 +649,20 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     float4* dst = reinterpret_cast<float4*>(tab);
     for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
     if (tid == 0) { evn[0] = 0; evn[1] = 0; }
+    // the chunk's received vectors and partial-layer lists (contiguous in global)
+    const int64_t g0 = c * a.V + v0;
+    for (int i = tid; i < vce * m; i += nth) ych[i] = load_y32(a, g0 * m + i);
+    const int lb = tparam.list_bytes;
+    if (lb) {
+      const uint8_t* lsrc = a.lists + g0 * lb;
+      if ((lb & 3) == 0) {
+        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(lsrc);
+        uint32_t* d4 = reinterpret_cast<uint32_t*>(lch);
+        for (int i = tid; i < vce * lb / 4; i += nth) d4[i] = s4[i];
+      } else {
+        for (int i = tid; i < vce * lb; i += nth) lch[i] = lsrc[i];
+      }
+    }
   }
   __syncthreads();
   const TabPtrs T = tab_ptrs(tab, m, N);
@@ -651,14 +681,13 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       const int vl = item * nvi + j;
       if (j >= nvi || vl >= vce) continue;
       const int64_t gv = gbase + vl;
+      const float2* ys = ych + vl * m;
       float yp = 0.f;
       for (int r = lane; r < m; r += 32) {
-        const float2 v = load_y32(a, gv * m + r);
-        ys[r] = v;
+        const float2 v = ys[r];
         yp = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, yp));
       }
       const float ynorm = sqrtf(warp_sum(yp)) * 1.0001f;
-      __syncwarp();
       float e2 = 0.f;
       if (lane < N) {
         const float2 z = rotate_row(tab, m, N, lane, [&](int r) { return ys[r]; });
@@ -670,8 +699,8 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         e2 = e * e;
       }
       eacc_v[j] = sqrtf(warp_sum(e2)) * 1.001f;
-      __syncwarp();
     }
+    __syncwarp();
 
     // ---- traversal over path batches ----
     Top3 run = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
@@ -693,17 +722,17 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
           ok[t] = vl[t] < nvi && item * nvi + vl[t] < vce;
         }
         if (!ok[t]) { vl[t] = 0; pp[t] = 0; }
-        gvl[t] = gbase + item * nvi + vl[t];
+        gvl[t] = item * nvi + vl[t];   // chunk-local vector (lists staged in smem)
       }
       float ped[PT], evp[PT];
       unsigned evm[PT];
-      traverse_paths<N, L, PT>(T, zs, thr, a.lists, tp, tp.list_bytes, vl, gvl, pp, ped, evm, evp);
+      traverse_paths<N, L, PT>(T, zs, thr, lch, tp, tp.list_bytes, vl, gvl, pp, ped, evm, evp);
       // log paths with a marked decision whose prefix may still be competitive
       const float bnd = (wb == INF) ? INF : wb + 2.f * ped_tol(wb, eacc_v[0], N);
 #pragma unroll
       for (int t = 0; t < PT; ++t) {
         if (ok[t] && evm[t] != 0u && evp[t] <= bnd) {
-          const int4 e4 = make_int4(pp[t], (int)evm[t], (int)gvl[t], EV_NODE);
+          const int4 e4 = make_int4(pp[t], (int)evm[t], (int)(gbase + gvl[t]), EV_NODE);
           const int idx = atomicAdd(evn, 1);
           if (idx < TRAV_EV_CAP) evb[idx] = e4;
           else log_event(a, e4);
