@@ -180,7 +180,7 @@ struct Workspace {
     vpath = o; o = up(o + 8 * B);
     events = o; o = up(o + 16 * ev_cap);
     lists = o; o = up(o + B * (int64_t)list_bytes);
-    zq = o; o = up(o + B * 8 * (int64_t)n);
+    zq = o; o = up(o + B * 16 * (int64_t)((n + 1) / 2));
     total = o;
   }
 };
@@ -290,7 +290,7 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   a.vpath = reinterpret_cast<int2*>(ws + W.vpath);
   a.events = reinterpret_cast<int4*>(ws + W.events);
   a.lists = reinterpret_cast<uint8_t*>(ws + W.lists);
-  a.zq = reinterpret_cast<float2*>(ws + W.zq);
+  a.zq = reinterpret_cast<float4*>(ws + W.zq);
   a.stats = g_stats;
   a.n_ch = n_ch;
   a.V = v_per_ch;

@@ -25,8 +25,9 @@ struct TableLayout {
   int off_qh;     // M x N float2  : Q^H transposed (fp32): qhT[r][k], for z = Q^H y
   int off_shift;  // N float2      : constant symbol offset folded into z
   int off_lay;    // N float4      : per layer (kneg, c2r, S_k, |shift_k|)
-  int off_rcol;   // N x NP float2 : column pos holds r''[k][pos], k < pos
-  int np_;        // column stride (N rounded up to even, for 128-bit loads)
+  int off_rcol;   // N columns x NPP float4: column pos, row pair q holds
+                  // {rr_2q, rr_2q+1, ri_2q, ri_2q+1} of r''[k][pos] (0 for k >= pos)
+  int npp;        // row pairs, (N+1)/2
   int total;      // floats per channel
 
   __host__ __device__ static int up4(int x) { return (x + 3) & ~3; }
@@ -35,8 +36,8 @@ struct TableLayout {
     off_shift = up4(off_qh + 2 * n * m);
     off_lay = up4(off_shift + 2 * n);
     off_rcol = up4(off_lay + 4 * n);
-    np_ = (n + 1) & ~1;
-    total = up4(off_rcol + 2 * n * np_);
+    npp = (n + 1) / 2;
+    total = up4(off_rcol + 4 * n * npp);
   }
 };
 

@@ -162,15 +162,16 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     tc[tl.off_qh + 2 * idx] = (float)q.x;
     tc[tl.off_qh + 2 * idx + 1] = (float)(-q.y);
   }
-  for (int idx = lane; idx < n * tl.np_; idx += 32) {
-    int pos = idx / tl.np_, k = idx % tl.np_;   // column pos, row k
+  for (int idx = lane; idx < n * 2 * tl.npp; idx += 32) {
+    const int pos = idx / (2 * tl.npp), k = idx % (2 * tl.npp);   // column pos, row k
     float2 v = make_float2(0.f, 0.f);
     if (k < pos) {
       double2 r = Rp[k * n + phys_of[pos]];
       v = make_float2((float)(sc * r.x), (float)(sc * r.y));
     }
-    tc[tl.off_rcol + 2 * idx] = v.x;
-    tc[tl.off_rcol + 2 * idx + 1] = v.y;
+    float* blk = tc + tl.off_rcol + 4 * (pos * tl.npp + (k >> 1));
+    blk[k & 1] = v.x;
+    blk[2 + (k & 1)] = v.y;
   }
   for (int k = lane; k < n; k += 32) {
     double sr = 0.0, si = 0.0, sabs = 0.0;

@@ -55,7 +55,7 @@ struct DetectArgs {
   int2* vpath;              // (B,) p1, p2
   int4* events;             // (ev_cap,) {path, mask|pos, vector, type}
   uint8_t* lists;           // (B, list_bytes) partial-layer selections
-  float2* zq;               // (B, N) z' as computed by the traversal kernel
+  float4* zq;               // (B, NPP) z' row pairs as computed by the traversal kernel
   int32_t* stats;           // diagnostics (may be null)
   int64_t n_ch, V;
   int m;
@@ -114,12 +114,33 @@ __device__ __forceinline__ float ped_step(float ped, float c2r, float fr, float 
   return __fmaf_rn(ei, ei, ped);
 }
 
+// scalar twin of the packed row-pair update in traverse_paths (same fmas, same order)
 __device__ __forceinline__ void acc_step(float& ar, float& ai, float rr, float ri, float fr,
                                          float fi) {
   ar = __fmaf_rn(rr, fr, ar);
-  ar = __fmaf_rn(-ri, fi, ar);
+  ar = __fmaf_rn(ri, -fi, ar);
   ai = __fmaf_rn(rr, fi, ai);
   ai = __fmaf_rn(ri, fr, ai);
+}
+
+// ---- packed f32x2 (Blackwell FFMA2: two IEEE fmas per lane per instruction) ----
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo32(u64 v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi32(u64 v) { return __uint_as_float((unsigned)(v >> 32)); }
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+// r''(row k, column pos) from the row-pair table
+__device__ __forceinline__ float2 rcol_at(const float* rcol, int npp, int k, int pos) {
+  const float* b = rcol + 4 * (pos * npp + (k >> 1));
+  return make_float2(b[k & 1], b[2 + (k & 1)]);
 }
 
 __device__ __forceinline__ float2 load_y32(const DetectArgs& a, int64_t idx) {
@@ -170,7 +191,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 struct TabPtrs {
   const float4* lay4;
-  const float* rcol;   // 16-byte aligned columns of NP float2
+  const float* rcol;   // 16-byte aligned columns of NPP float4 row pairs
 };
 
 __device__ __forceinline__ TabPtrs tab_ptrs(const float* tab, int m, int n) {
@@ -183,31 +204,39 @@ __device__ __forceinline__ TabPtrs tab_ptrs(const float* tab, int m, int n) {
 
 // K3 inner loop: NS independent paths.  Per path: PED, mask of layers whose
 // decision was within the bound, PED prefix at the first such layer.
-template <int N, int L, int NS>
-__device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float2* __restrict__ zs,
+// Accumulators are row pairs in f32x2 registers: each 128-bit LDS of r''
+// ({rr_2q, rr_2q+1, ri_2q, ri_2q+1}) feeds 4 FFMA2 = 8 fmas per path.
+// zs: per vector NPP float4 {re_2q, re_2q+1, im_2q, im_2q+1}.
+// LAB (NS == 1): record level indices lab[pos] and PED prefix pre[pos] and
+// stop after layer `stop` (phase re-traces).
+template <int N, int L, int NS, bool GUARD, bool LAB>
+__device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* __restrict__ zs,
                                                const float* __restrict__ thr,
                                                const uint8_t* __restrict__ lists,
                                                const TreeParams& tp, int list_bytes,
                                                const int (&vl)[NS], const int64_t (&gvl)[NS],
                                                const int (&p)[NS], float (&ped)[NS],
-                                               unsigned (&evm)[NS], float (&evp)[NS]) {
-  constexpr int NP = (N + 1) & ~1;
+                                               unsigned (&evm)[NS], float (&evp)[NS],
+                                               int* lab = nullptr, float* pre = nullptr,
+                                               int stop = -1) {
+  constexpr int NPP = (N + 1) / 2;
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
   const float INF = __int_as_float(0x7f800000);
-  float ar[NS][N], ai[NS][N];
+  u64 arp[NS][NPP], aip[NS][NPP], ped2[NS], evp2[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const float2 z = zs[vl[s] * N + k];
-      ar[s][k] = z.x;
-      ai[s][k] = z.y;
+    for (int q = 0; q < NPP; ++q) {
+      const float4 z = zs[vl[s] * NPP + q];
+      arp[s][q] = pk2(z.x, z.y);
+      aip[s][q] = pk2(z.z, z.w);
     }
-    ped[s] = 0.f;
+    ped2[s] = 0ull;
     evm[s] = 0u;
-    evp[s] = INF;
+    evp2[s] = pk2(INF, INF);
   }
   const int top_lo = N - tp.n_top;   // layers pos >= top_lo are expanded (n_top <= XM)
+  const ulonglong2* rcol2 = reinterpret_cast<const ulonglong2*>(T.rcol);
 #pragma unroll
   for (int pos = N - 1; pos >= 0; --pos) {
     const float4 ly = T.lay4[pos];
@@ -224,79 +253,75 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float2* _
     } else {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const float th = thr[vl[s] * N + pos];
+        const float ur = (pos & 1) ? hi32(arp[s][pos >> 1]) : lo32(arp[s][pos >> 1]);
+        const float ui = (pos & 1) ? hi32(aip[s][pos >> 1]) : lo32(aip[s][pos >> 1]);
         float tr, ti;
-        fr[s] = slice_axis<L>(ar[s][pos], kneg, tr);
-        fi[s] = slice_axis<L>(ai[s][pos], kneg, ti);
-        const bool near = fabsf(tr) > th || fabsf(ti) > th;
-        evm[s] |= near ? (1u << pos) : 0u;
-        evp[s] = near ? fminf(evp[s], ped[s]) : evp[s];
+        fr[s] = slice_axis<L>(ur, kneg, tr);
+        fi[s] = slice_axis<L>(ui, kneg, ti);
+        if (GUARD) {
+          const float th = thr[vl[s] * N + pos];
+          const bool near = fabsf(tr) > th || fabsf(ti) > th;
+          const bool first = near && evm[s] == 0u;
+          evm[s] |= near ? (1u << pos) : 0u;
+          evp2[s] = first ? ped2[s] : evp2[s];
+        }
       }
     }
+    if (LAB) {
+      lab[pos] = (int)fr[0] * 8 + (int)fi[0];
+      pre[pos] = lo32(ped2[0]) + hi32(ped2[0]);
+      if (pos == stop) return;
+    }
 #pragma unroll
-    for (int s = 0; s < NS; ++s) ped[s] = ped_step(ped[s], c2r, fr[s], fi[s], ar[s][pos], ai[s][pos]);
+    for (int s = 0; s < NS; ++s) {
+      const float ur = (pos & 1) ? hi32(arp[s][pos >> 1]) : lo32(arp[s][pos >> 1]);
+      const float ui = (pos & 1) ? hi32(aip[s][pos >> 1]) : lo32(aip[s][pos >> 1]);
+      const float er = __fmaf_rn(c2r, fr[s], ur);
+      const float ei = __fmaf_rn(c2r, fi[s], ui);
+      const u64 e2 = pk2(er, ei);
+      ped2[s] = ffma2(e2, e2, ped2[s]);
+    }
     // push this layer's symbols into the rows below: acc_k += r''_k,pos * s
-    const float4* rc = reinterpret_cast<const float4*>(T.rcol + 2 * NP * pos);
+    const ulonglong2* rc = rcol2 + pos * NPP;
 #pragma unroll
-    for (int k = 0; k < pos; k += 2) {
-      const float4 r2 = rc[k >> 1];
+    for (int q = 0; q < (pos + 1) / 2; ++q) {
+      const ulonglong2 r = rc[q];          // .x = (rr, rr'), .y = (ri, ri')
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        acc_step(ar[s][k], ai[s][k], r2.x, r2.y, fr[s], fi[s]);
-        if (k + 1 < pos) acc_step(ar[s][k + 1], ai[s][k + 1], r2.z, r2.w, fr[s], fi[s]);
+        const u64 fr2 = pk2(fr[s], fr[s]), fi2 = pk2(fi[s], fi[s]), nfi2 = pk2(-fi[s], -fi[s]);
+        arp[s][q] = ffma2(r.x, fr2, arp[s][q]);
+        arp[s][q] = ffma2(r.y, nfi2, arp[s][q]);
+        aip[s][q] = ffma2(r.x, fi2, aip[s][q]);
+        aip[s][q] = ffma2(r.y, fr2, aip[s][q]);
       }
     }
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    ped[s] = lo32(ped2[s]) + hi32(ped2[s]);
+    evp[s] = lo32(evp2[s]) + hi32(evp2[s]);
   }
 }
 
 // Single-path re-trace with the identical arithmetic: level indices lab[pos]
 // (ir*8+ii) and the PED prefix pre[pos] before layer pos, for pos >= stop.
+// zs: this vector's NPP float4 row pairs.  vlist: this vector's lists.
 template <int N, int L>
-__device__ __forceinline__ void retrace_inline(const float* tab, int m, const float2* zs,
+__device__ __forceinline__ void retrace_inline(const float* tab, int m, const float4* zs,
                                                const uint8_t* vlist, const TreeParams& tp, int p,
                                                int stop, int* lab, float* pre) {
-  constexpr int NP = (N + 1) & ~1;
-  constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
   const TabPtrs T = tab_ptrs(tab, m, N);
-  float ar[N], ai[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    ar[k] = zs[k].x;
-    ai[k] = zs[k].y;
-  }
-  float ped = 0.f;
-  const int top_lo = N - tp.n_top;
-#pragma unroll
-  for (int pos = N - 1; pos >= 0; --pos) {
-    const float4 ly = T.lay4[pos];
-    float fr, fi;
-    if (pos >= N - XM && pos >= top_lo) {
-      int ir, ii;
-      expanded_symbol<L>(tp, pos, p, vlist, ir, ii);
-      fr = (float)ir;
-      fi = (float)ii;
-    } else {
-      float tr, ti;
-      fr = slice_axis<L>(ar[pos], ly.x, tr);
-      fi = slice_axis<L>(ai[pos], ly.x, ti);
-    }
-    lab[pos] = (int)fr * 8 + (int)fi;
-    pre[pos] = ped;
-    if (pos == stop) return;
-    ped = ped_step(ped, ly.y, fr, fi, ar[pos], ai[pos]);
-    const float4* rc = reinterpret_cast<const float4*>(T.rcol + 2 * NP * pos);
-#pragma unroll
-    for (int k = 0; k < pos; k += 2) {
-      const float4 r2 = rc[k >> 1];
-      acc_step(ar[k], ai[k], r2.x, r2.y, fr, fi);
-      if (k + 1 < pos) acc_step(ar[k + 1], ai[k + 1], r2.z, r2.w, fr, fi);
-    }
-  }
+  const int vl[1] = {0}, pp[1] = {p};
+  const int64_t gvl[1] = {0};
+  float ped[1], evp[1];
+  unsigned evm[1];
+  traverse_paths<N, L, 1, false, true>(T, zs, nullptr, vlist, tp, 0, vl, gvl, pp, ped, evm, evp,
+                                       lab, pre, stop);
 }
 
 // out-of-line copy for the rare paths (ties, events)
 template <int N, int L>
-static __device__ __noinline__ void retrace_path(const float* tab, int m, const float2* zs,
+static __device__ __noinline__ void retrace_path(const float* tab, int m, const float4* zs,
                                                  const uint8_t* vlist, const TreeParams& tp, int p,
                                                  int stop, int* lab, float* pre) {
   retrace_inline<N, L>(tab, m, zs, vlist, tp, p, stop, lab, pre);
@@ -319,7 +344,7 @@ template <int N>
 struct TravCfg {
   static constexpr int PT = N <= 8 ? MPNL_PT_SMALL : (N <= 16 ? MPNL_PT_MID : MPNL_PT_LARGE);
   static constexpr int MAXT = 128;                       // threads per CTA
-  static constexpr int MINB = PT * N <= 48 ? 4 : (PT * N <= 64 ? 3 : 2);   // CTAs per SM
+  static constexpr int MINB = PT * N <= 24 ? 4 : 3;      // CTAs per SM (no spills)
 };
 
 // ---------------------------------------------------------------------------
@@ -473,7 +498,6 @@ __device__ __forceinline__ void group_top3(Top3 t, int width, float& b1, unsigne
 template <int N, int L>
 __global__ void __launch_bounds__(128)
 select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
-  constexpr int NP = (N + 1) & ~1;
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
   __shared__ TreeParams tp;
   __shared__ float scratch[20 * 128];
@@ -523,7 +547,7 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
 #pragma unroll
     for (int q2 = 0; q2 < q; ++q2) {
       const int l = N - 1 - q2;
-      const float2 r2 = reinterpret_cast<const float2*>(T.rcol + 2 * NP * l)[j];
+      const float2 r2 = rcol_at(T.rcol, (N + 1) / 2, j, l);
       acc_step(ar_, ai_, r2.x, r2.y, sr[q2], si[q2]);
     }
     if (j > pos) pedp = ped_step(pedp, T.lay4[j].y, sr[q], si[q], ar_, ai_);
@@ -601,14 +625,15 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
 // K3: traversal (hot kernel)
 // ===========================================================================
 struct TravSmem {
-  int tpo, tab, wz, wthr, wy, ev, evn, ylist, lists, total_bytes;
+  int tpo, tab, wz, wthr, weac, wy, ev, evn, ylist, lists, total_bytes;
   __host__ __device__ TravSmem(int m, int n, int warps, int vc, int list_bytes) {
     TableLayout tl(m, n);
     int o = 0;
     tpo = o; o += TableLayout::up4((int)(sizeof(TreeParams) / 4));
     tab = o; o += tl.total;
-    wz = o; o += warps * 2 * MPNL_VPI_MAX * n;     // per warp z' (VPI x N float2)
+    wz = o; o += warps * 4 * MPNL_VPI_MAX * ((n + 1) / 2);   // per warp z' (VPI x NPP float4)
     wthr = o; o += warps * MPNL_VPI_MAX * n;       // per warp thresholds
+    weac = o; o += warps * MPNL_VPI_MAX;           // per warp E_acc per vector
     wy = o; o += 0;                                // (unused)
     ev = o; o += 4 * TRAV_EV_CAP;                  // int4 event buffer
     evn = o; o += 4;
@@ -635,8 +660,10 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   const float INF = __int_as_float(0x7f800000);
   TreeParams& tp = *reinterpret_cast<TreeParams*>(sm + so.tpo);
   float* tab = sm + so.tab;
-  float2* zs = reinterpret_cast<float2*>(sm + so.wz) + warp * MPNL_VPI_MAX * N;
+  constexpr int NPP = (N + 1) / 2;
+  float4* zs = reinterpret_cast<float4*>(sm + so.wz) + warp * MPNL_VPI_MAX * NPP;
   float* thr = sm + so.wthr + warp * MPNL_VPI_MAX * N;
+  float* weacc = sm + so.weac + warp * MPNL_VPI_MAX;
   float2* ych = reinterpret_cast<float2*>(sm + so.ylist);
   uint8_t* lch = reinterpret_cast<uint8_t*>(sm) + so.lists;
   int4* evb = reinterpret_cast<int4*>(sm + so.ev);
@@ -674,12 +701,11 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
 
   for (int item = warp; item < items; item += nw) {
     // ---- prologue per vector: z' (lane = row), per-layer bounds, E_acc ----
-    float eacc_v[MPNL_VPI_MAX];
-#pragma unroll
-    for (int j = 0; j < MPNL_VPI_MAX; ++j) {
-      eacc_v[j] = 0.f;
+    // (not unrolled: one copy of the rotation code keeps the I-cache for the hot loop)
+#pragma unroll 1
+    for (int j = 0; j < nvi; ++j) {
       const int vl = item * nvi + j;
-      if (j >= nvi || vl >= vce) continue;
+      if (vl >= vce) break;
       const int64_t gv = gbase + vl;
       const float2* ys = ych + vl * m;
       float yp = 0.f;
@@ -691,17 +717,22 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       float e2 = 0.f;
       if (lane < N) {
         const float2 z = rotate_row(tab, m, N, lane, [&](int r) { return ys[r]; });
-        zs[j * N + lane] = z;
-        a.zq[gv * N + lane] = z;
+        // row-pair layout {re_2q, re_2q+1, im_2q, im_2q+1}
+        float* zf = reinterpret_cast<float*>(zs + j * NPP) + 4 * (lane >> 1) + (lane & 1);
+        zf[0] = z.x;
+        zf[2] = z.y;
+        float* zg = reinterpret_cast<float*>(a.zq + gv * NPP) + 4 * (lane >> 1) + (lane & 1);
+        zg[0] = z.x;
+        zg[2] = z.y;
         const float4 ly = T.lay4[lane];
         const float e = row_bound(ynorm, z, ly, lane, m, N, L, a.guard_scale);
         thr[j * N + lane] = 0.5f - e / ly.y - MPNL_U * 2.f * L;
         e2 = e * e;
       }
-      eacc_v[j] = sqrtf(warp_sum(e2)) * 1.001f;
+      const float ea = sqrtf(warp_sum(e2)) * 1.001f;
+      if (lane == 0) weacc[j] = ea;
     }
     __syncwarp();
-
     // ---- traversal over path batches ----
     Top3 run = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
     float wb = INF;   // warp-wide best so far of this vector (batch mode)
@@ -726,9 +757,10 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       }
       float ped[PT], evp[PT];
       unsigned evm[PT];
-      traverse_paths<N, L, PT>(T, zs, thr, lch, tp, tp.list_bytes, vl, gvl, pp, ped, evm, evp);
+      traverse_paths<N, L, PT, true, false>(T, zs, thr, lch, tp, tp.list_bytes, vl, gvl, pp, ped,
+                                            evm, evp);
       // log paths with a marked decision whose prefix may still be competitive
-      const float bnd = (wb == INF) ? INF : wb + 2.f * ped_tol(wb, eacc_v[0], N);
+      const float bnd = (wb == INF) ? INF : wb + 2.f * ped_tol(wb, weacc[0], N);
 #pragma unroll
       for (int t = 0; t < PT; ++t) {
         if (ok[t] && evm[t] != 0u && evp[t] <= bnd) {
@@ -758,11 +790,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
           const int j = t0 / g;
           const int vlj = item * nvi + j;
           if (lane == 0 && j < nvi && vlj < vce) {
-            float ej = 0.f;
-#pragma unroll
-            for (int jj = 0; jj < MPNL_VPI_MAX; ++jj)
-              if (jj == j) ej = eacc_v[jj];
-            a.vres[gbase + vlj] = make_float4(b1, b2, b3, ej);
+            a.vres[gbase + vlj] = make_float4(b1, b2, b3, weacc[j]);
             a.vpath[gbase + vlj] = make_int2((int)q1, (int)q2);
           }
         }
@@ -777,11 +805,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
           const int j = (t * 32 + lane) / P;
           const int vlj = item * nvi + j;
           if ((lane % P) == 0 && j < nvi && vlj < vce) {
-            float ej = 0.f;
-#pragma unroll
-            for (int jj = 0; jj < MPNL_VPI_MAX; ++jj)
-              if (jj == j) ej = eacc_v[jj];
-            a.vres[gbase + vlj] = make_float4(b1, b2, b3, ej);
+            a.vres[gbase + vlj] = make_float4(b1, b2, b3, weacc[j]);
             a.vpath[gbase + vlj] = make_int2((int)q1, (int)q2);
           }
         }
@@ -792,7 +816,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       unsigned q1, q2;
       warp_top3(run, b1, q1, b2, q2, b3);
       if (lane == 0) {
-        a.vres[gbase + item] = make_float4(b1, b2, b3, eacc_v[0]);
+        a.vres[gbase + item] = make_float4(b1, b2, b3, weacc[0]);
         a.vpath[gbase + item] = make_int2((int)q1, (int)q2);
       }
     }
@@ -826,14 +850,15 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int vec_blocks) {
   const TableLayout tl(m, N);
   const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
   const int64_t B = a.n_ch * a.V;
-  float2 zl[N];
+  constexpr int NPP = (N + 1) / 2;
+  float4 zl[NPP];
   int lab[N];
   float pre[N];
   auto prep = [&](int64_t gv, const float*& tab) {
     const int64_t c = gv / a.V;
     tab = a.tables + c * (int64_t)tl.total;
 #pragma unroll
-    for (int k = 0; k < N; ++k) zl[k] = a.zq[gv * N + k];
+    for (int q = 0; q < NPP; ++q) zl[q] = a.zq[gv * NPP + q];
     return c;
   };
   if ((int)blockIdx.x < vec_blocks) {
