@@ -22,8 +22,8 @@ namespace mpnl {
 // --------------------------------------------------------------------------
 struct TableLayout {
   int m, n;
-  int off_qh;     // M x N float2  : Q^H transposed (fp32): qhT[r][k], for z = Q^H y
-  int off_shift;  // N float2      : constant symbol offset folded into z
+  int off_qh;     // M x N double2 : Q^H transposed (fp64): qhT[r][k], for z = Q^H y
+  int off_shift;  // N double2     : constant symbol offset folded into z (fp64)
   int off_lay;    // N float4      : per layer (kneg, c2r, S_k, |shift_k|)
   int off_rcol;   // N columns x NPP float4: column pos, row pair q holds
                   // {rr_2q, rr_2q+1, ri_2q, ri_2q+1} of r''[k][pos] (0 for k >= pos)
@@ -33,8 +33,8 @@ struct TableLayout {
   __host__ __device__ static int up4(int x) { return (x + 3) & ~3; }
   __host__ __device__ TableLayout(int m_, int n_) : m(m_), n(n_) {
     off_qh = 0;
-    off_shift = up4(off_qh + 2 * n * m);
-    off_lay = up4(off_shift + 2 * n);
+    off_shift = up4(off_qh + 4 * n * m);
+    off_lay = up4(off_shift + 4 * n);
     off_rcol = up4(off_lay + 4 * n);
     npp = (n + 1) / 2;
     total = up4(off_rcol + 4 * n * npp);

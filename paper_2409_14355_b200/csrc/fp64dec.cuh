@@ -9,8 +9,30 @@
 
 namespace mpnl {
 
+// (L-1-2i)/norm exactly as the reference computes its points (a division),
+// folded at compile time: no DDIV at run time.
 __device__ __forceinline__ double level_value(int i, int L, double nrm) {
-  return (double)(L - 1 - 2 * i) / nrm;
+  (void)nrm;
+  constexpr double n2 = 1.4142135623730951, n4 = 3.1622776601683795, n8 = 6.48074069840786;
+  if (L == 2) return i == 0 ? 1.0 / n2 : -1.0 / n2;
+  if (L == 4) {
+    switch (i) {
+      case 0: return 3.0 / n4;
+      case 1: return 1.0 / n4;
+      case 2: return -1.0 / n4;
+      default: return -3.0 / n4;
+    }
+  }
+  switch (i) {
+    case 0: return 7.0 / n8;
+    case 1: return 5.0 / n8;
+    case 2: return 3.0 / n8;
+    case 3: return 1.0 / n8;
+    case 4: return -1.0 / n8;
+    case 5: return -3.0 / n8;
+    case 6: return -5.0 / n8;
+    default: return -7.0 / n8;
+  }
 }
 
 static __device__ __noinline__ int nearest_level_f64(double c, int L, double nrm) {

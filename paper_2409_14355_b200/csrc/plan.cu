@@ -156,11 +156,11 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
   const double nrm = qam_norm_d(L);
   const double sc = 2.0 / nrm;
   const double lv = (double)(L - 1) / nrm;
+  double2* qt = reinterpret_cast<double2*>(tc + tl.off_qh);
   for (int idx = lane; idx < n * m; idx += 32) {
     int r = idx / n, k = idx % n;       // transposed: qhT[r][k] = conj(q_k[r])
     double2 q = A[r * n + phys_of[k]];
-    tc[tl.off_qh + 2 * idx] = (float)q.x;
-    tc[tl.off_qh + 2 * idx + 1] = (float)(-q.y);
+    qt[idx] = make_double2(q.x, -q.y);
   }
   for (int idx = lane; idx < n * 2 * tl.npp; idx += 32) {
     const int pos = idx / (2 * tl.npp), k = idx % (2 * tl.npp);   // column pos, row k
@@ -183,8 +183,7 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     }
     // shift = (L-1)(1+i)/norm * sum_{j>=k} r_kj
     double shr = lv * (sr - si), shi = lv * (sr + si);
-    tc[tl.off_shift + 2 * k] = (float)shr;
-    tc[tl.off_shift + 2 * k + 1] = (float)shi;
+    reinterpret_cast<double2*>(tc + tl.off_shift)[k] = make_double2(shr, shi);
     double rkk = Rp[k * n + phys_of[k]].x;
     double c2r = sc * rkk;
     float* ly = tc + tl.off_lay + 4 * k;

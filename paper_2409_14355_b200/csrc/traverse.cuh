@@ -151,31 +151,38 @@ __device__ __forceinline__ float2 load_y32(const DetectArgs& a, int64_t idx) {
   return reinterpret_cast<const float2*>(a.y)[idx];
 }
 
-// z'_k = (Q^H y)_k - shift_k in fp32 (identical sequence everywhere)
+// z'_k = fl32((Q^H y)_k - shift_k): rotation in fp64, one rounding at the end
+// (identical sequence everywhere).  yat(r) returns y_r as float2.
 template <typename YF>
 __device__ __forceinline__ float2 rotate_row(const float* tab, int m, int n, int k, YF yat) {
   const TableLayout tl(m, n);
-  const float2* qt = reinterpret_cast<const float2*>(tab + tl.off_qh);
-  float zr = 0.f, zi = 0.f;
+  const double2* qt = reinterpret_cast<const double2*>(tab + tl.off_qh);
+  double zr = 0.0, zi = 0.0;
   for (int r = 0; r < m; ++r) {
-    const float2 q = qt[r * n + k], yv = yat(r);
-    zr = __fmaf_rn(q.x, yv.x, zr);
-    zr = __fmaf_rn(-q.y, yv.y, zr);
-    zi = __fmaf_rn(q.x, yv.y, zi);
-    zi = __fmaf_rn(q.y, yv.x, zi);
+    const double2 q = qt[r * n + k];
+    const float2 yv = yat(r);
+    const double yr = yv.x, yi = yv.y;
+    zr = fma(q.x, yr, zr);
+    zr = fma(-q.y, yi, zr);
+    zi = fma(q.x, yi, zi);
+    zi = fma(q.y, yr, zi);
   }
-  const float2 sh = reinterpret_cast<const float2*>(tab + tl.off_shift)[k];
-  return make_float2(__fsub_rn(zr, sh.x), __fsub_rn(zi, sh.y));
+  const double2 sh = reinterpret_cast<const double2*>(tab + tl.off_shift)[k];
+  return make_float2((float)(zr - sh.x), (float)(zi - sh.y));
 }
 
 // acc-domain fp32 error bound of row k's decision variable:
-//   u [ (2M+1) sqrt2 |y| + |z'_k| + |shift_k| + (2(N-1-k)+1) (|z'_k| + (L-1) S_k) ]
+//   u [ c_y sqrt2 |y| + (2(N-1-k)+2) (|z'_k| + (L-1) S_k) ] + 1e-12 |y|
+// (c_y = 1 when y arrived in fp64 and was rounded to fp32; the fp64 rotation
+//  itself contributes ~1e-16 |y|)
 __device__ __forceinline__ float row_bound(float ynorm, float2 zk, float4 lyk, int k, int m, int n,
-                                           int L, float gs) {
+                                           int L, float gs, int y_f64) {
+  (void)m;
   const float za = fmaxf(fabsf(zk.x), fabsf(zk.y));
   const float xk = za + (float)(L - 1) * lyk.z;
-  return gs * MPNL_U * 1.01f *
-         ((2.f * m + 1.f) * 1.4142136f * ynorm + za + lyk.w + (2.f * (n - 1 - k) + 1.f) * xk);
+  return gs * (MPNL_U * 1.01f * ((y_f64 ? 1.4142136f * ynorm : 0.f) +
+                                 (2.f * (n - 1 - k) + 2.f) * xk) +
+               1e-12f * ynorm);
 }
 
 // fp32 PED error bound from the L2 norm of the per-layer acc bounds
@@ -561,8 +568,9 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
     yn = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, yn));
   }
   const float4 lyp = T.lay4[pos];
-  const float E = row_bound(sqrtf(yn) * 1.0001f, zpos, lyp, pos, m, N, L, a.guard_scale) / lyp.y +
-                  MPNL_U * 2.f * L;
+  const float E =
+      row_bound(sqrtf(yn) * 1.0001f, zpos, lyp, pos, m, N, L, a.guard_scale, a.y_f64) / lyp.y +
+      MPNL_U * 2.f * L;
   // centre in level-index units (unclamped)
   const float cx = __fmul_rn(__fmul_rn(xr, lyp.x), (float)(L - 1));
   const float cy = __fmul_rn(__fmul_rn(xi, lyp.x), (float)(L - 1));
@@ -725,7 +733,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         zg[0] = z.x;
         zg[2] = z.y;
         const float4 ly = T.lay4[lane];
-        const float e = row_bound(ynorm, z, ly, lane, m, N, L, a.guard_scale);
+        const float e = row_bound(ynorm, z, ly, lane, m, N, L, a.guard_scale, a.y_f64);
         thr[j * N + lane] = 0.5f - e / ly.y - MPNL_U * 2.f * L;
         e2 = e * e;
       }
@@ -891,18 +899,20 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int vec_blocks) {
     }
     float corr = 0.f;
     if (a.metric_offset) {
-      const float2* sh = reinterpret_cast<const float2*>(tab + tl.off_shift);
-      float yn = 0.f, zn = 0.f;
+      const double2* sh = reinterpret_cast<const double2*>(tab + tl.off_shift);
+      double yn = 0.0, zn = 0.0;
       for (int r = 0; r < m; ++r) {
         const float2 v = load_y32(a, gv * m + r);
-        yn = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, yn));
+        yn = fma((double)v.x, (double)v.x, fma((double)v.y, (double)v.y, yn));
       }
+      const float* zf = reinterpret_cast<const float*>(zl);
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        const float zr = zl[k].x + sh[k].x, zi = zl[k].y + sh[k].y;
-        zn = __fmaf_rn(zr, zr, __fmaf_rn(zi, zi, zn));
+        const double zr = zf[4 * (k >> 1) + (k & 1)] + sh[k].x;
+        const double zi = zf[4 * (k >> 1) + 2 + (k & 1)] + sh[k].y;
+        zn = fma(zr, zr, fma(zi, zi, zn));
       }
-      corr = yn - zn;
+      corr = (float)(yn - zn);
     }
     const int32_t* pc = a.perm + c * N;
     uint8_t* out = a.hard + gv * N;
