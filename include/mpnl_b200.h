@@ -100,9 +100,10 @@ int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64,
  * the rigorous bound; <= 0 restores the default).  Diagnostics only. */
 void mpnl_set_guard_scale(double c);
 
-/* Optional device int32[4] counters: [0] += guard events logged, [1] +=
- * events re-decided in fp64, [2] += near-ties resolved in fp64, [3] +=
- * vectors sent to the fp64 kernel (NULL disables).  Diagnostics only. */
+/* Optional device int32[8] counters (NULL disables; diagnostics only):
+ * [1] guarded decisions re-decided in fp64, [2] two-way near-ties settled in
+ * fp64, [3] vectors sent to the fp64 kernel, of which [4] three-way ties,
+ * [5] fp64-level ties, [6] fp64 disagreements, [7] event-log overflows. */
 void mpnl_set_stats(int32_t* device_counters);
 
 /* FFMA throughput probe (for the roofline denominator): runs `iters` dependent

@@ -341,10 +341,13 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
       e = launch_fast(n, L, 1, a, tp, (unsigned)(n_ch * chunks), threads, so.total_bytes, 0, st);
       if (e != cudaSuccess) return cuda_fail(e, "traverse kernel");
     } else {
-      // first vb blocks: one thread per vector; as many again for the events
+      // winners: one thread per vector; then events/ties: one warp per event
       const int64_t vb = (B + 127) / 128;
-      e = launch_fast(n, L, 2, a, tp, (unsigned)(2 * vb), 128, 0, (int)vb, st);
+      e = launch_fast(n, L, 2, a, tp, (unsigned)vb, 128, 0, 0, st);
       if (e != cudaSuccess) return cuda_fail(e, "verify kernel");
+      const int64_t cb = std::min<int64_t>(std::max<int64_t>((B + 255) / 256, 1), 148 * 16);
+      e = launch_fast(n, L, 3, a, tp, (unsigned)cb, 128, 0, 0, st);
+      if (e != cudaSuccess) return cuda_fail(e, "check kernel");
     }
     return MPNL_OK;
   }
@@ -366,14 +369,15 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   ea.hard = hard;
   ea.metric = metric;
   int grid;
+  // one CTA per vector (grid-stride over the task list)
   if (slow) {
     ea.list = nullptr;
     ea.n_tasks = B;
-    grid = (int)std::min<int64_t>((B + 3) / 4, 148 * 16);
+    grid = (int)std::min<int64_t>(B, 148 * 8);
   } else {
     ea.list = a.fix_list;
     ea.count = a.counters;
-    grid = (int)std::min<int64_t>((B + 3) / 4, 148 * 4);
+    grid = 148 * 8;
   }
   e = launch_exact(ea, tp, grid, st);
   if (e != cudaSuccess) return cuda_fail(e, "exact kernel");
@@ -427,7 +431,7 @@ int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64, con
   ea.full_metrics = metrics;
   ea.full_best = best;
   ea.exact_order = 1;
-  const int grid = (int)std::min<int64_t>((B + 3) / 4, 148 * 16);
+  const int grid = (int)std::min<int64_t>(B, 148 * 8);
   cudaError_t e = launch_exact(ea, tb.tp, grid, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "exact kernel");
   return MPNL_OK;

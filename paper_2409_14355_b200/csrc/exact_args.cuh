@@ -27,18 +27,4 @@ struct ExactArgs {
   int exact_order;         // 1: full layers in stable distance order too
 };
 
-#define EX_WARPS 4
-
-struct ExSmem {
-  int acc, z, lab, blab, total;   // offsets in bytes, per warp
-  __host__ __device__ ExSmem(int n) {
-    int o = 0;
-    acc = o; o += 32 * n * 16;
-    z = o; o += n * 16;
-    lab = o; o += 32 * 32;   // current path labels (stream order), per lane
-    blab = o; o += 32 * 32;  // best-so-far labels per lane
-    total = (o + 15) & ~15;
-  }
-};
-
 }  // namespace mpnl

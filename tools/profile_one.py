@@ -17,7 +17,7 @@ c = constellation_for(cfg.order)
 h = torch.from_numpy(d["h"]).cuda()
 y = torch.from_numpy(d["y"]).cuda()
 from paper_2409_14355_b200 import _lib
-stats = torch.zeros(4, dtype=torch.int32, device="cuda")
+stats = torch.zeros(8, dtype=torch.int32, device="cuda")
 _lib.load().mpnl_set_stats(stats.data_ptr())
 for _ in range(reps):
     plan = det.mpnl_plan_batch(h, float(d["nv"][0]), cfg.n_paths, c)
@@ -25,5 +25,5 @@ for _ in range(reps):
 torch.cuda.synchronize()
 nv_ = y.shape[0] * y.shape[1]
 print(name, "vectors", nv_, "flag rate", float(flags.float().mean()),
-      "per vector: events logged %.3f checked %.3f ties %.4f flagged %.4f" % tuple(
-          x / reps / nv_ for x in stats.tolist()))
+      "per vector: checked %.3f ties %.4f flagged %.5f [3way %.5f f64tie %.5f mismatch %.5f overflow %.5f]" % tuple(
+          x / reps / nv_ for x in stats.tolist()[1:]))
