@@ -166,7 +166,7 @@ cudaError_t launch_fast(int n, int L, int kind, const DetectArgs& a, const TreeP
 
 // Workspace carve-up (byte offsets), identical in mpnl_workspace_bytes and the launches.
 struct Workspace {
-  int64_t counters, fix_list, vflag, vres, vpath, events, lists, zq, total;
+  int64_t counters, fix_list, vflag, vres, vpath, events, lists, zq, thrg, vaux, total;
   int64_t ev_cap;
   Workspace(int64_t B, int list_bytes, int n) {
     auto up = [](int64_t x) { return (x + 255) & ~int64_t(255); };
@@ -181,6 +181,8 @@ struct Workspace {
     events = o; o = up(o + 16 * ev_cap);
     lists = o; o = up(o + B * (int64_t)list_bytes);
     zq = o; o = up(o + B * 16 * (int64_t)((n + 1) / 2));
+    thrg = o; o = up(o + B * 4 * (int64_t)n);
+    vaux = o; o = up(o + B * 8);
     total = o;
   }
 };
@@ -291,6 +293,8 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   a.events = reinterpret_cast<int4*>(ws + W.events);
   a.lists = reinterpret_cast<uint8_t*>(ws + W.lists);
   a.zq = reinterpret_cast<float4*>(ws + W.zq);
+  a.thrg = reinterpret_cast<float*>(ws + W.thrg);
+  a.vaux = reinterpret_cast<float2*>(ws + W.vaux);
   a.stats = g_stats;
   a.n_ch = n_ch;
   a.V = v_per_ch;
@@ -308,6 +312,14 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     if (e == cudaSuccess) e = cudaMemsetAsync(a.vflag, 0, 4 * B, st);
     if (e != cudaSuccess) return cuda_fail(e, "memset");
     if (slow) return MPNL_OK;
+    // per-vector preparation (z', guard thresholds), one warp per vector
+    {
+      const int64_t pch = (v_per_ch + PREP_VC - 1) / PREP_VC;
+      if (n_ch * pch > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
+      const PrepSmem ps(m, n);
+      e = launch_fast(n, L, 4, a, tp, (unsigned)(n_ch * pch), 128, ps.total, (int)pch, st);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "prep kernel");
     for (int pos = n - 1; pos >= n - tp.n_top; --pos) {
       if (tp.e[pos] == L * L) continue;
       const int64_t items = B * (tp.n_paths / tp.stride[pos + 1]);

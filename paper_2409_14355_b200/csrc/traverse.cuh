@@ -55,7 +55,9 @@ struct DetectArgs {
   int2* vpath;              // (B,) p1, p2
   int4* events;             // (ev_cap,) {path, mask|pos, vector, type}
   uint8_t* lists;           // (B, list_bytes) partial-layer selections
-  float4* zq;               // (B, NPP) z' row pairs as computed by the traversal kernel
+  float4* zq;               // (B, NPP) z' row pairs (prep kernel)
+  float* thrg;              // (B, N) per-layer index-domain guard thresholds (prep kernel)
+  float2* vaux;             // (B,) E_acc (L2 over layers), metric offset ||y||^2-||z||^2
   int32_t* stats;           // diagnostics (may be null)
   int64_t n_ch, V;
   int m;
@@ -188,6 +190,12 @@ __device__ __forceinline__ float row_bound(float ynorm, float2 zk, float4 lyk, i
 // fp32 PED error bound from the L2 norm of the per-layer acc bounds
 __device__ __forceinline__ float ped_tol(float b, float eacc, int n) {
   return 2.f * sqrtf(b) * eacc + eacc * eacc + 2.f * n * MPNL_U * b;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -429,6 +437,99 @@ __device__ __forceinline__ void group_top3(Top3 t, int width, float& b1, unsigne
 }
 
 // ===========================================================================
+// K1b: per-vector preparation.  CTA = a channel's chunk of PREP_VC vectors:
+// the channel's fp64 Q^H (transposed), shift and layer table are staged once;
+// thread per (vector, row):  z'_k = fl32((Q^H y)_k - shift_k) with the rotation
+// in fp64, the per-layer guard threshold of the fp32 traversal; then thread per
+// vector: E_acc (L2 over layers) and the M > N metric offset (fixed-order sums).
+// ===========================================================================
+#define PREP_VC 32
+
+struct PrepSmem {
+  int qt, sh, ly, y, e2, zn, total;   // bytes
+  __host__ __device__ PrepSmem(int m, int n) {
+    int o = 0;
+    qt = o; o += 16 * m * n;
+    sh = o; o += 16 * n;
+    ly = o; o += 16 * n;
+    y = o; o += 16 * PREP_VC * m;
+    e2 = o; o += 8 * PREP_VC * n;
+    zn = o; o += 8 * PREP_VC * n;
+    total = o;
+  }
+};
+
+template <int N, int L>
+__global__ void __launch_bounds__(128)
+prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
+  (void)tparam;
+  constexpr int NPP = (N + 1) / 2;
+  extern __shared__ __align__(16) uint8_t psm[];
+  const int m = a.m;
+  const PrepSmem so(m, N);
+  double2* qt = reinterpret_cast<double2*>(psm + so.qt);
+  double2* sh = reinterpret_cast<double2*>(psm + so.sh);
+  float4* ly = reinterpret_cast<float4*>(psm + so.ly);
+  double2* ys = reinterpret_cast<double2*>(psm + so.y);
+  double* e2s = reinterpret_cast<double*>(psm + so.e2);
+  double* zns = reinterpret_cast<double*>(psm + so.zn);
+  const TableLayout tl(m, N);
+  const int64_t c = blockIdx.x / chunks;
+  const int v0 = (blockIdx.x % chunks) * PREP_VC;
+  const int vce = (int)min((int64_t)PREP_VC, a.V - v0);
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const float* tab = a.tables + c * (int64_t)tl.total;
+  {
+    const double2* q = reinterpret_cast<const double2*>(tab + tl.off_qh);
+    for (int i = tid; i < m * N; i += nth) qt[i] = q[i];
+    const double2* s2 = reinterpret_cast<const double2*>(tab + tl.off_shift);
+    const float4* l4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
+    for (int i = tid; i < N; i += nth) { sh[i] = s2[i]; ly[i] = l4[i]; }
+    const int64_t y0 = (c * a.V + v0) * (int64_t)m;
+    for (int i = tid; i < vce * m; i += nth) {
+      if (a.y_f64) {
+        ys[i] = reinterpret_cast<const double2*>(a.y)[y0 + i];
+      } else {
+        const float2 v = reinterpret_cast<const float2*>(a.y)[y0 + i];
+        ys[i] = make_double2(v.x, v.y);
+      }
+    }
+  }
+  __syncthreads();
+  // ||y|| per vector (fixed order), needed only for the tiny fp64 term of the bound
+  for (int it = tid; it < vce * N; it += nth) {
+    const int v = it / N, k = it - v * N;
+    const double2* yv = ys + v * m;
+    double zr = 0.0, zi = 0.0, yn = 0.0;
+    for (int r = 0; r < m; ++r) {
+      const double2 q = qt[r * N + k], y = yv[r];
+      zr = fma(q.x, y.x, zr);
+      zr = fma(-q.y, y.y, zr);
+      zi = fma(q.x, y.y, zi);
+      zi = fma(q.y, y.x, zi);
+      yn = fma(y.x, y.x, fma(y.y, y.y, yn));
+    }
+    const int64_t gv = c * a.V + v0 + v;
+    const float2 z = make_float2((float)(zr - sh[k].x), (float)(zi - sh[k].y));
+    float* zg = reinterpret_cast<float*>(a.zq + gv * NPP) + 4 * (k >> 1) + (k & 1);
+    zg[0] = z.x;
+    zg[2] = z.y;
+    const float e = row_bound((float)sqrt(yn) * 1.0001f, z, ly[k], k, m, N, L, a.guard_scale, 0);
+    a.thrg[gv * N + k] = 0.5f - e / ly[k].y - MPNL_U * 2.f * L;
+    e2s[v * N + k] = (double)e * e;
+    zns[v * N + k] = zr * zr + zi * zi;
+  }
+  __syncthreads();
+  for (int v = tid; v < vce; v += nth) {
+    const double2* yv = ys + v * m;
+    double yn = 0.0, e2 = 0.0, zn = 0.0;
+    for (int r = 0; r < m; ++r) yn = fma(yv[r].x, yv[r].x, fma(yv[r].y, yv[r].y, yn));
+    for (int k = 0; k < N; ++k) { e2 += e2s[v * N + k]; zn += zns[v * N + k]; }
+    a.vaux[c * a.V + v0 + v] = make_float2((float)sqrt(e2) * 1.001f, (float)(yn - zn));
+  }
+}
+
+// ===========================================================================
 // K2: partial-layer selection lists, one thread per (vector, parent)
 // ===========================================================================
 template <int N, int L>
@@ -458,7 +559,7 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
   const TabPtrs T = tab_ptrs(tab, m, N);
   const int p0 = par * tp.stride[pos + 1];
   uint8_t* vlist = a.lists + gv * tp.list_bytes;
-  auto yat = [&](int r) { return load_y32(a, gv * m + r); };
+  const float* zrow = reinterpret_cast<const float*>(a.zq + gv * ((N + 1) / 2));
   // prefix symbols (expanded layers above pos)
   float sr[XM], si[XM];
 #pragma unroll
@@ -471,35 +572,25 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
       sr[q] = (float)ir; si[q] = (float)ii;
     }
   }
-  // acc at each prefix layer and at pos (traversal order), PED prefix
-  float pedp = 0.f, xr = 0.f, xi = 0.f;
-  float2 zpos = make_float2(0.f, 0.f);
+  // acc at pos in traversal order (z' from the prep kernel)
+  float xr = 0.f, xi = 0.f;
 #pragma unroll
   for (int q = 0; q < XM; ++q) {
     const int j = N - 1 - q;
-    if (j < pos) break;
-    const float2 zj = rotate_row(tab, m, N, j, yat);
-    float ar_ = zj.x, ai_ = zj.y;
+    if (j != pos) continue;
+    float ar_ = zrow[4 * (j >> 1) + (j & 1)], ai_ = zrow[4 * (j >> 1) + 2 + (j & 1)];
 #pragma unroll
     for (int q2 = 0; q2 < q; ++q2) {
       const int l = N - 1 - q2;
       const float2 r2 = rcol_at(T.rcol, (N + 1) / 2, j, l);
       acc_step(ar_, ai_, r2.x, r2.y, sr[q2], si[q2]);
     }
-    if (j > pos) pedp = ped_step(pedp, T.lay4[j].y, sr[q], si[q], ar_, ai_);
-    else { xr = ar_; xi = ai_; zpos = zj; }
-  }
-  (void)pedp;
-  // error bound of the centre (index units) for the cut guard
-  float yn = 0.f;
-  for (int r = 0; r < m; ++r) {
-    const float2 v = yat(r);
-    yn = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, yn));
+    xr = ar_;
+    xi = ai_;
   }
   const float4 lyp = T.lay4[pos];
-  const float E =
-      row_bound(sqrtf(yn) * 1.0001f, zpos, lyp, pos, m, N, L, a.guard_scale, a.y_f64) / lyp.y +
-      MPNL_U * 2.f * L;
+  // index-domain centre error bound (prep kernel) for the cut guard
+  const float E = 0.5f - a.thrg[gv * N + pos];
   // centre in level-index units (unclamped)
   const float cx = __fmul_rn(__fmul_rn(xr, lyp.x), (float)(L - 1));
   const float cy = __fmul_rn(__fmul_rn(xi, lyp.x), (float)(L - 1));
@@ -574,7 +665,7 @@ struct TravSmem {
     wy = o; o += 0;                                // (unused)
     ev = o; o += 4 * TRAV_EV_CAP;                  // int4 event buffer
     evn = o; o += 4;
-    ylist = o; o += TableLayout::up4(2 * vc * m); // the chunk's y (fp32)
+    ylist = o; o += 0;
     lists = o * 4;                                 // the chunk's selection lists (bytes)
     total_bytes = lists + ((vc * list_bytes + 15) & ~15);
   }
@@ -601,7 +692,6 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   float4* zs = reinterpret_cast<float4*>(sm + so.wz) + warp * MPNL_VPI_MAX * NPP;
   float* thr = sm + so.wthr + warp * MPNL_VPI_MAX * N;
   float* weacc = sm + so.weac + warp * MPNL_VPI_MAX;
-  float2* ych = reinterpret_cast<float2*>(sm + so.ylist);
   uint8_t* lch = reinterpret_cast<uint8_t*>(sm) + so.lists;
   int4* evb = reinterpret_cast<int4*>(sm + so.ev);
   int* evn = reinterpret_cast<int*>(sm + so.evn);
@@ -613,9 +703,8 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     float4* dst = reinterpret_cast<float4*>(tab);
     for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
     if (tid == 0) { evn[0] = 0; evn[1] = 0; }
-    // the chunk's received vectors and partial-layer lists (contiguous in global)
+    // the chunk's partial-layer lists (contiguous in global)
     const int64_t g0 = c * a.V + v0;
-    for (int i = tid; i < vce * m; i += nth) ych[i] = load_y32(a, g0 * m + i);
     const int lb = tparam.list_bytes;
     if (lb) {
       const uint8_t* lsrc = a.lists + g0 * lb;
@@ -637,37 +726,15 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   const int64_t gbase = c * a.V + v0;
 
   for (int item = warp; item < items; item += nw) {
-    // ---- prologue per vector: z' (lane = row), per-layer bounds, E_acc ----
-    // (not unrolled: one copy of the rotation code keeps the I-cache for the hot loop)
+    // ---- prologue: the item's z' rows, guard thresholds, E_acc (prep kernel) ----
 #pragma unroll 1
     for (int j = 0; j < nvi; ++j) {
       const int vl = item * nvi + j;
       if (vl >= vce) break;
       const int64_t gv = gbase + vl;
-      const float2* ys = ych + vl * m;
-      float yp = 0.f;
-      for (int r = lane; r < m; r += 32) {
-        const float2 v = ys[r];
-        yp = __fmaf_rn(v.x, v.x, __fmaf_rn(v.y, v.y, yp));
-      }
-      const float ynorm = sqrtf(warp_sum(yp)) * 1.0001f;
-      float e2 = 0.f;
-      if (lane < N) {
-        const float2 z = rotate_row(tab, m, N, lane, [&](int r) { return ys[r]; });
-        // row-pair layout {re_2q, re_2q+1, im_2q, im_2q+1}
-        float* zf = reinterpret_cast<float*>(zs + j * NPP) + 4 * (lane >> 1) + (lane & 1);
-        zf[0] = z.x;
-        zf[2] = z.y;
-        float* zg = reinterpret_cast<float*>(a.zq + gv * NPP) + 4 * (lane >> 1) + (lane & 1);
-        zg[0] = z.x;
-        zg[2] = z.y;
-        const float4 ly = T.lay4[lane];
-        const float e = row_bound(ynorm, z, ly, lane, m, N, L, a.guard_scale, a.y_f64);
-        thr[j * N + lane] = 0.5f - e / ly.y - MPNL_U * 2.f * L;
-        e2 = e * e;
-      }
-      const float ea = sqrtf(warp_sum(e2)) * 1.001f;
-      if (lane == 0) weacc[j] = ea;
+      if (lane < NPP) zs[j * NPP + lane] = a.zq[gv * NPP + lane];
+      if (lane < N) thr[j * N + lane] = a.thrg[gv * N + lane];
+      if (lane == 0) weacc[j] = a.vaux[gv].x;
     }
     __syncwarp();
     // ---- traversal over path batches ----
@@ -813,23 +880,7 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
     else
       log_event(a, make_int4(pth.x, pth.y, (int)gv, EV_TIE));
   }
-  float corr = 0.f;
-  if (a.metric_offset) {
-    const double2* sh = reinterpret_cast<const double2*>(tab + tl.off_shift);
-    double yn = 0.0, zn = 0.0;
-    for (int r = 0; r < m; ++r) {
-      const float2 v = load_y32(a, gv * m + r);
-      yn = fma((double)v.x, (double)v.x, fma((double)v.y, (double)v.y, yn));
-    }
-    const float* zf = reinterpret_cast<const float*>(zl);
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const double zr = zf[4 * (k >> 1) + (k & 1)] + sh[k].x;
-      const double zi = zf[4 * (k >> 1) + 2 + (k & 1)] + sh[k].y;
-      zn = fma(zr, zr, fma(zi, zi, zn));
-    }
-    corr = (float)(yn - zn);
-  }
+  const float corr = a.metric_offset ? a.vaux[gv].y : 0.f;
   const int32_t* pc = a.perm + c * N;
   uint8_t* out = a.hard + gv * N;
 #pragma unroll
@@ -848,12 +899,6 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
 // The fp32 re-trace is warp-cooperative (lane = tree row) with exactly the
 // traversal's per-row fma sequence, so it reproduces the traversal bit for bit.
 // ===========================================================================
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // fp32 re-trace of path p with lanes = rows; labw[pos] / prew[pos] (smem) for pos >= stop
 template <int N, int L>
 __device__ __forceinline__ void warp_retrace(const float* tab, int m, const float4* zrow,

@@ -8,7 +8,7 @@
 namespace mpnl {
 
 // kind 0 = select_kernel (extra = layer), 1 = traverse_kernel, 2 = verify_kernel,
-// 3 = check_kernel
+// 3 = check_kernel, 4 = prep_kernel
 template <int NN, int L>
 cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp, unsigned grid,
                             int threads, size_t smem, int extra, cudaStream_t st) {
@@ -18,6 +18,10 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
     auto k = traverse_kernel<NN, L>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<grid, threads, smem, st>>>(a, tp);
+  } else if (kind == 4) {
+    auto k = prep_kernel<NN, L>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, threads, smem, st>>>(a, tp, extra);
   } else if (kind == 2) {
     verify_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
   } else {
