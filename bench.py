@@ -45,6 +45,19 @@ def _peaks():
         return {}
 
 
+def _traffic(cfg_name, n_rb, full_rb):
+    """DRAM bytes per launch of the traversal kernel from the committed ncu
+    capture summary (profiles/traffic.json, written by tools/ncu_summary.py
+    traffic); only valid for the full-size workload it was captured on."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())[cfg_name]
+    except Exception:
+        return None, None
+    if n_rb != full_rb:
+        return None, None
+    return t["dram_bytes_per_launch"], t["source"]
+
+
 # ---------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
@@ -147,6 +160,30 @@ def _cpu_model():
 
 
 # ---------------------------------------------------------------------------
+# multi-rank plumbing (replicas over RB shards; no data-path collective)
+# ---------------------------------------------------------------------------
+
+def rank_seed(seed, rank):
+    """Each rank detects its own seeded copy of the workload (weak scaling)."""
+    return seed + 7919 * rank
+
+
+def max_over_ranks(x, world, device=None):
+    """Max of a per-rank scalar (device time) over all ranks."""
+    if world == 1:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_rate(vectors_per_rank, world, total_ms, steps):
+    """Whole-job vectors/s: all ranks' vectors / the slowest rank's time."""
+    return world * vectors_per_rank / (total_ms / steps * 1e-3)
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 
@@ -163,7 +200,7 @@ def run_gpu(args, rank, world):
     cfg = CONFIGS[args.config]
     c = constellation_for(cfg.order)
     n_rb = args.n_rb or cfg.n_rb
-    d = generate(cfg, seed=args.seed + 7919 * rank, n_rb=n_rb)
+    d = generate(cfg, seed=rank_seed(args.seed, rank), n_rb=n_rb)
     nv = float(d["nv"][0])
     h_host = torch.from_numpy(d["h"]).pin_memory()
     y_host = torch.from_numpy(d["y"]).pin_memory()
@@ -231,14 +268,11 @@ def run_gpu(args, rank, world):
             torch.cuda.synchronize()
             step_ms.append(ev[0].elapsed_time(ev[3]))
             k_ms.append(ev[1].elapsed_time(ev[2]))
-    tot_ms = float(np.sum(step_ms))
+    tot_ms = max_over_ranks(float(np.sum(step_ms)), world, dev)
     if world > 1:
-        t = torch.tensor([tot_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_ms = float(t.item())
         torch.distributed.barrier()
     ms_per_step = tot_ms / args.steps
-    value = world * nvec / (ms_per_step * 1e-3)
+    value = job_rate(nvec, world, tot_ms, args.steps)
 
     # e2e through the public API from pinned host buffers
     out_h = torch.empty(hard.shape, dtype=torch.uint8).pin_memory()
@@ -259,12 +293,8 @@ def run_gpu(args, rank, world):
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e_ms.append(a0.elapsed_time(a1))
-    e2e_tot = float(np.sum(e2e_ms))
-    if world > 1:
-        t = torch.tensor([e2e_tot], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_tot = float(t.item())
-    e2e_val = world * nvec / (e2e_tot / args.steps * 1e-3)
+    e2e_tot = max_over_ranks(float(np.sum(e2e_ms)), world, dev)
+    e2e_val = job_rate(nvec, world, e2e_tot, args.steps)
     h2d = h_host.numel() * h_host.element_size() + y_host.numel() * y_host.element_size()
     d2h = out_h.numel() + out_m.numel() * 4
 
@@ -274,6 +304,7 @@ def run_gpu(args, rank, world):
     k_avg = float(np.mean(k_ms))
     achieved = flops_vec * nvec / (k_avg * 1e-3) / 1e12
     peak = max(SPEC_FP32_TFLOPS, probe_tflops)
+    traffic, traffic_src = _traffic(cfg.name, n_rb, cfg.n_rb)
     line = {
         "metric": "detected MIMO vectors/sec",
         "value": round(value, 1),
@@ -295,7 +326,9 @@ def run_gpu(args, rank, world):
         "gbit_per_s": round(value * cfg.n * (cfg.order.bit_length() - 1) / 1e9, 3),
         "flag_rate": flag_rate,
         "roofline": {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes": round(cfg.bytes_per_vector() * nvec),
                      "kernel": f"traverse_kernel<{cfg.n},{int(round(c.order ** 0.5))}>",
                      "kernel_ms": round(k_avg, 4),
                      "flops_per_vector": flops_vec,

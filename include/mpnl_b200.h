@@ -66,7 +66,7 @@ int64_t mpnl_workspace_bytes(int64_t n_vectors, int n, int q,
  * stream order and metric (n_ch*v_per_ch) float32 = ||y - H x_hat||^2.
  * expansions: host array of n int64 (from mpnl_alloc_expansions).
  * flags (optional, may be NULL): 1 where the fp32 pass was re-done in fp64.
- * Launches the fp32 traversal kernel, then the fp64 fix-up kernel. */
+ * Launches stages 1-4 of mpnl_detect_hard_stage in order (no host sync). */
 int mpnl_detect_hard(const int32_t* perm, const void* r64, const void* qh64,
                      const float* tables, const void* y, int y_is_f64,
                      int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
@@ -75,9 +75,10 @@ int mpnl_detect_hard(const int32_t* perm, const void* r64, const void* qh64,
                      void* workspace, int64_t workspace_bytes, void* stream);
 
 /* The stages of mpnl_detect_hard, for timing (all four, in order, equal
- * mpnl_detect_hard): 1 = reset + partial-layer selection kernel, 2 = fp32
- * traversal kernel (the hot kernel), 3 = verification kernel (winner labels,
- * fp64 re-decision of guarded decisions), 4 = fp64 fix-up kernel. */
+ * mpnl_detect_hard): 1 = reset + fp64 rotation/guard-bound kernel +
+ * partial-layer selection kernel, 2 = fp32 traversal kernel (the hot kernel),
+ * 3 = verification kernel (winner labels, near-ties) + fp64 re-decision of
+ * guarded decisions, 4 = fp64 fix-up kernel (+ flags). */
 int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64,
                            const void* qh64, const float* tables, const void* y,
                            int y_is_f64, int64_t n_ch, int64_t v_per_ch, int m,
