@@ -125,7 +125,7 @@ TreeBuild build_tree(int n, int L, const int64_t* ex) {
     b.tp.ms[pos] = div_magic((unsigned)b.tp.stride[pos]);
     b.tp.me[pos] = div_magic((unsigned)b.tp.e[pos]);
   }
-  b.tp.list_bytes = off;
+  b.tp.list_bytes = (off + 15) & ~15;   // 16-byte rows (cp.async staging)
   b.ok = true;
   return b;
 }
@@ -181,7 +181,7 @@ struct Workspace {
     events = o; o = up(o + 16 * ev_cap);
     lists = o; o = up(o + B * (int64_t)list_bytes);
     zq = o; o = up(o + B * 16 * (int64_t)((n + 1) / 2));
-    thrg = o; o = up(o + B * 4 * (int64_t)n);
+    thrg = o; o = up(o + B * 4 * (int64_t)((n + 3) & ~3));
     vaux = o; o = up(o + B * 8);
     total = o;
   }
@@ -305,7 +305,8 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   // overloaded channels and trees with more than MPNL_XMAX expanded layers
   // (e.g. full enumeration) are detected entirely by the fp64 kernel
   const bool augmented = n > m;
-  const bool slow = augmented || tp.n_top > MPNL_XMAX;
+  const bool slow = augmented || tp.n_top > MPNL_XMAX ||
+                    TravSmem(m, n, 4, MPNL_VPI_MAX, tp.list_bytes).total_bytes > 160 * 1024;
   cudaError_t e = cudaSuccess;
   if (stage == 1) {   // reset + partial-layer selection
     e = cudaMemsetAsync(a.counters, 0, 16, st);
@@ -338,19 +339,12 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     a.vpi = vpi;
     a.bpv = bpv;
     const int threads = 128, warps = threads / 32;
-    // vectors per CTA: 4 work items per warp (many small CTAs keep every SM fed;
-    // the per-CTA table staging is a few KB)
-    const int unit = (bpv > 1 || vpi == 1 ? 1 : vpi) * warps;
-    int64_t vc = std::min<int64_t>(4 * unit, v_per_ch);
-    while (vc > unit && TravSmem(m, n, warps, (int)vc, tp.list_bytes).total_bytes > 56 * 1024)
-      vc -= unit;
-    const int64_t chunks = (v_per_ch + vc - 1) / vc;
-    if (n_ch * chunks > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
-    a.vc = (int)vc;
-    a.chunks = (int)chunks;
+    const int nvi = (bpv > 1 || vpi == 1) ? 1 : vpi;
+    const int64_t items = n_ch * ((v_per_ch + nvi - 1) / nvi);
+    if (items > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "too many work items");
     if (stage == 2) {
-      const TravSmem so(m, n, warps, (int)vc, tp.list_bytes);
-      e = launch_fast(n, L, 1, a, tp, (unsigned)(n_ch * chunks), threads, so.total_bytes, 0, st);
+      const TravSmem so(m, n, warps, nvi, tp.list_bytes);
+      e = launch_fast(n, L, 1, a, tp, 0, threads, so.total_bytes, (int)items, st);
       if (e != cudaSuccess) return cuda_fail(e, "traverse kernel");
     } else {
       // winners: one thread per vector; then events/ties: one warp per event

@@ -24,9 +24,9 @@ struct TableLayout {
   int m, n;
   int off_qh;     // M x N double2 : Q^H transposed (fp64): qhT[r][k], for z = Q^H y
   int off_shift;  // N double2     : constant symbol offset folded into z (fp64)
-  int off_lay;    // N float4      : per layer (kneg, c2r, S_k, |shift_k|)
+  int off_lay;    // N float4      : per layer (kx = -1/c2r, c2r, S_k, |shift_k|)
   int off_rcol;   // N columns x NPP float4: column pos, row pair q holds
-                  // {rr_2q, rr_2q+1, ri_2q, ri_2q+1} of r''[k][pos] (0 for k >= pos)
+                  // {rr_2q, ri_2q, rr_2q+1, ri_2q+1} of r''[k][pos] (0 for k >= pos)
   int npp;        // row pairs, (N+1)/2
   int total;      // floats per channel
 
@@ -49,7 +49,7 @@ struct TreeParams {
   int e[MPNL_MAX_N];           // expansions by tree position
   int stride[MPNL_MAX_N + 1];  // prod_{j<pos} e_j (stride[N] = P)
   int list_off[MPNL_MAX_N];    // byte offset of the partial-layer list (per vector)
-  int list_bytes;              // total list bytes per vector
+  int list_bytes;              // list bytes per vector (stride, multiple of 16)
   unsigned ms[MPNL_MAX_N];     // magic for p / stride[pos]   (fast_div)
   unsigned me[MPNL_MAX_N];     // magic for d / e[pos]
 };

@@ -169,9 +169,9 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
       double2 r = Rp[k * n + phys_of[pos]];
       v = make_float2((float)(sc * r.x), (float)(sc * r.y));
     }
-    float* blk = tc + tl.off_rcol + 4 * (pos * tl.npp + (k >> 1));
-    blk[k & 1] = v.x;
-    blk[2 + (k & 1)] = v.y;
+    float* blk = tc + tl.off_rcol + 4 * (pos * tl.npp + (k >> 1)) + 2 * (k & 1);
+    blk[0] = v.x;   // {rr_2q, ri_2q, rr_2q+1, ri_2q+1}
+    blk[1] = v.y;
   }
   for (int k = lane; k < n; k += 32) {
     double sr = 0.0, si = 0.0, sabs = 0.0;
@@ -187,7 +187,7 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     double rkk = Rp[k * n + phys_of[k]].x;
     double c2r = sc * rkk;
     float* ly = tc + tl.off_lay + 4 * k;
-    ly[0] = (float)(-1.0 / (c2r * (L - 1)));
+    ly[0] = (float)(-1.0 / c2r);   // kx: acc -> level-index units
     ly[1] = (float)c2r;
     // guard inputs: S_k = sum_{j>k} |Re r''| + |Im r''| (as stored) and |shift_k|
     ly[2] = (float)(sabs * (1.0 + 1e-6));

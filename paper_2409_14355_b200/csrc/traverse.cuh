@@ -63,7 +63,6 @@ struct DetectArgs {
   int m;
   int y_f64;
   int ev_cap;
-  int vc, chunks;           // traverse: vectors per CTA, chunks per channel
   int vpi, bpv;             // vectors per warp item (VPI mode) / path batches per vector
   int metric_offset;        // 1 when M > N: add ||y||^2 - ||z||^2
   float guard_scale;        // scales the fp32 error bound (1 = rigorous)
@@ -71,11 +70,12 @@ struct DetectArgs {
 
 #define MPNL_XMAX 3             // expanded (e > 1) layers handled by the fast path
 #define MPNL_VPI_MAX 8          // vectors per warp item in VPI mode
-#define MPNL_MAGIC 8388608.0f   // 2^23: fma(a, L-1, 2^23) rounds a to an integer
+#define MPNL_MAGIC 12582912.0f  // 1.5 * 2^23: fma(acc, kx, MAGIC) rounds x to an integer
 #define MPNL_U 5.9604645e-08f   // 2^-24
 #define EV_NODE 0
 #define EV_CUT 1
 #define TRAV_EV_CAP 256         // per-CTA event buffer of the traversal kernel
+#define MPNL_XS_STRIDE 128      // = traversal threads per CTA (per-thread symbol slots)
 
 // ---------------------------------------------------------------------------
 // arithmetic shared by all kernels: keeping it in one place makes the
@@ -98,14 +98,16 @@ __device__ __forceinline__ void expanded_symbol(const TreeParams& tp, int pos, i
   }
 }
 
-// slice one axis: a' = sat(acc * kneg), i = round(a' (L-1)); t = a'(L-1) - i
+// slice one axis: x = acc * kx (level-index units, kx = -1/c2r), n = round(x)
+// by the 1.5 * 2^23 magic number (exact for |x| < 2^22), t = x - n, symbol =
+// clamp(n, 0, L-1).  The packed twin in traverse_paths performs the very same
+// per-element operations (fma, sub, fma, min, max), so both are bit-identical.
 template <int L>
-__device__ __forceinline__ float slice_axis(float acc, float kneg, float& t) {
-  const float s = __saturatef(__fmul_rn(acc, kneg));
-  const float mm = __fmaf_rn(s, (float)(L - 1), MPNL_MAGIC);
-  const float f = __fsub_rn(mm, MPNL_MAGIC);
-  t = __fmaf_rn(s, (float)(L - 1), -f);
-  return f;
+__device__ __forceinline__ float slice_axis(float acc, float kx, float& t) {
+  const float mm = __fmaf_rn(acc, kx, MPNL_MAGIC);
+  const float nf = __fsub_rn(MPNL_MAGIC, mm);   // -n
+  t = __fmaf_rn(acc, kx, nf);
+  return fmaxf(fminf(-nf, (float)(L - 1)), 0.f);
 }
 
 __device__ __forceinline__ float ped_step(float ped, float c2r, float fr, float fi, float ur,
@@ -139,10 +141,28 @@ __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
+__device__ __forceinline__ u64 fsub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// ---- cp.async (LDGSTS): global -> shared without staging registers ----
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
 // r''(row k, column pos) from the row-pair table
 __device__ __forceinline__ float2 rcol_at(const float* rcol, int npp, int k, int pos) {
-  const float* b = rcol + 4 * (pos * npp + (k >> 1));
-  return make_float2(b[k & 1], b[2 + (k & 1)]);
+  const float* b = rcol + 4 * (pos * npp + (k >> 1)) + 2 * (k & 1);
+  return make_float2(b[0], b[1]);
 }
 
 __device__ __forceinline__ float2 load_y32(const DetectArgs& a, int64_t idx) {
@@ -219,12 +239,16 @@ __device__ __forceinline__ TabPtrs tab_ptrs(const float* tab, int m, int n) {
 
 // K3 inner loop: NS independent paths.  Per path: PED, mask of layers whose
 // decision was within the bound, PED prefix at the first such layer.
-// Accumulators are row pairs in f32x2 registers: each 128-bit LDS of r''
-// ({rr_2q, rr_2q+1, ri_2q, ri_2q+1}) feeds 4 FFMA2 = 8 fmas per path.
-// zs: per vector NPP float4 {re_2q, re_2q+1, im_2q, im_2q+1}.
+// Accumulators are per row (re, im) f32x2 registers.  Slicing, the PED step
+// and the interference update are all packed: the update of row k is
+//   acc_k = FFMA2(rr_k (bcast), f, acc_k);  acc_k = FFMA2(-f.swap (lo only), ri_k (bcast), acc_k)
+// i.e. per element exactly acc_step's fma sequence, with no register moves
+// (the swap and the partial negation are free FFMA2 operand modifiers).
+// One 128-bit LDS of r'' ({rr_2q, ri_2q, rr_2q+1, ri_2q+1}) feeds 4 FFMA2 per path.
+// zs: per vector NPP float4 {re_2q, im_2q, re_2q+1, im_2q+1}.
 // LAB (NS == 1): record level indices lab[pos] and PED prefix pre[pos] and
 // stop after layer `stop` (phase re-traces).
-template <int N, int L, int NS, bool GUARD, bool LAB>
+template <int N, int L, int NS, bool GUARD, bool LAB, bool SAMEV = false>
 __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* __restrict__ zs,
                                                const float* __restrict__ thr,
                                                const uint8_t* __restrict__ lists,
@@ -233,49 +257,68 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
                                                const int (&p)[NS], float (&ped)[NS],
                                                unsigned (&evm)[NS], float (&evp)[NS],
                                                int* lab = nullptr, float* pre = nullptr,
-                                               int stop = -1) {
+                                               int stop = -1, const u64* xs = nullptr) {
   constexpr int NPP = (N + 1) / 2;
+  constexpr int N4 = (N + 3) & ~3;
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
   const float INF = __int_as_float(0x7f800000);
-  u64 arp[NS][NPP], aip[NS][NPP], ped2[NS], evp2[NS];
+  u64 acc[NS][2 * NPP], ped2[NS], evp2[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
 #pragma unroll
     for (int q = 0; q < NPP; ++q) {
-      const float4 z = zs[vl[s] * NPP + q];
-      arp[s][q] = pk2(z.x, z.y);
-      aip[s][q] = pk2(z.z, z.w);
+      const float4 z = zs[(SAMEV ? 0 : vl[s]) * NPP + q];
+      acc[s][2 * q] = pk2(z.x, z.y);
+      acc[s][2 * q + 1] = pk2(z.z, z.w);
     }
     ped2[s] = 0ull;
     evm[s] = 0u;
     evp2[s] = pk2(INF, INF);
   }
   const int top_lo = N - tp.n_top;   // layers pos >= top_lo are expanded (n_top <= XM)
-  const ulonglong2* rcol2 = reinterpret_cast<const ulonglong2*>(T.rcol);
+  const float4* rc4 = reinterpret_cast<const float4*>(T.rcol);
+  const u64 MAGIC2 = pk2(MPNL_MAGIC, MPNL_MAGIC);
 #pragma unroll
   for (int pos = N - 1; pos >= 0; --pos) {
     const float4 ly = T.lay4[pos];
-    const float kneg = ly.x, c2r = ly.y;
-    float fr[NS], fi[NS];
+    const float kx = ly.x, c2r = ly.y;
+    u64 f2[NS];
     if (pos >= N - XM && pos >= top_lo) {
+      if (xs != nullptr) {
+        // per-lane precomputed symbols (paths fixed per lane): a float pair for
+        // a full layer, the list index for a partial one
+        const bool full = tp.e[pos] == L * L;
 #pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        int ir, ii;
-        expanded_symbol<L>(tp, pos, p[s], lists + gvl[s] * list_bytes, ir, ii);
-        fr[s] = (float)ir;
-        fi[s] = (float)ii;
+        for (int s = 0; s < NS; ++s) {
+          const u64 x = xs[((N - 1 - pos) * NS + s) * MPNL_XS_STRIDE];
+          if (full) {
+            f2[s] = x;
+          } else {
+            const unsigned b = lists[(SAMEV ? 0 : (int)gvl[s]) * list_bytes + (int)(unsigned)x];
+            f2[s] = pk2((float)(b >> 3), (float)(b & 7u));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          int ir, ii;
+          expanded_symbol<L>(tp, pos, p[s], lists + gvl[s] * list_bytes, ir, ii);
+          f2[s] = pk2((float)ir, (float)ii);
+        }
       }
     } else {
+      // packed slicing of (re, im): the per-element twin of slice_axis
+      const u64 kx2 = pk2(kx, kx);
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const float ur = (pos & 1) ? hi32(arp[s][pos >> 1]) : lo32(arp[s][pos >> 1]);
-        const float ui = (pos & 1) ? hi32(aip[s][pos >> 1]) : lo32(aip[s][pos >> 1]);
-        float tr, ti;
-        fr[s] = slice_axis<L>(ur, kneg, tr);
-        fi[s] = slice_axis<L>(ui, kneg, ti);
+        const u64 mm = ffma2(acc[s][pos], kx2, MAGIC2);
+        const u64 nf = fsub2(MAGIC2, mm);
+        f2[s] = pk2(fmaxf(fminf(-lo32(nf), (float)(L - 1)), 0.f),
+                    fmaxf(fminf(-hi32(nf), (float)(L - 1)), 0.f));
         if (GUARD) {
-          const float th = thr[vl[s] * N + pos];
-          const bool near = fabsf(tr) > th || fabsf(ti) > th;
+          const u64 t2 = ffma2(acc[s][pos], kx2, nf);
+          const float th = thr[(SAMEV ? 0 : vl[s]) * N4 + pos];
+          const bool near = fmaxf(fabsf(lo32(t2)), fabsf(hi32(t2))) > th;
           const bool first = near && evm[s] == 0u;
           evm[s] |= near ? (1u << pos) : 0u;
           evp2[s] = first ? ped2[s] : evp2[s];
@@ -283,31 +326,29 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
       }
     }
     if (LAB) {
-      lab[pos] = (int)fr[0] * 8 + (int)fi[0];
+      lab[pos] = (int)lo32(f2[0]) * 8 + (int)hi32(f2[0]);
       pre[pos] = lo32(ped2[0]) + hi32(ped2[0]);
       if (pos == stop) return;
     }
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      const float ur = (pos & 1) ? hi32(arp[s][pos >> 1]) : lo32(arp[s][pos >> 1]);
-      const float ui = (pos & 1) ? hi32(aip[s][pos >> 1]) : lo32(aip[s][pos >> 1]);
-      const float er = __fmaf_rn(c2r, fr[s], ur);
-      const float ei = __fmaf_rn(c2r, fi[s], ui);
-      const u64 e2 = pk2(er, ei);
+      const u64 e2 = ffma2(pk2(c2r, c2r), f2[s], acc[s][pos]);   // c2r f + u
       ped2[s] = ffma2(e2, e2, ped2[s]);
     }
     // push this layer's symbols into the rows below: acc_k += r''_k,pos * s
-    const ulonglong2* rc = rcol2 + pos * NPP;
+    const float4* rc = rc4 + pos * NPP;
 #pragma unroll
     for (int q = 0; q < (pos + 1) / 2; ++q) {
-      const ulonglong2 r = rc[q];          // .x = (rr, rr'), .y = (ri, ri')
+      const float4 r = rc[q];              // {rr_2q, ri_2q, rr_2q+1, ri_2q+1}
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const u64 fr2 = pk2(fr[s], fr[s]), fi2 = pk2(fi[s], fi[s]), nfi2 = pk2(-fi[s], -fi[s]);
-        arp[s][q] = ffma2(r.x, fr2, arp[s][q]);
-        arp[s][q] = ffma2(r.y, nfi2, arp[s][q]);
-        aip[s][q] = ffma2(r.x, fi2, aip[s][q]);
-        aip[s][q] = ffma2(r.y, fr2, aip[s][q]);
+        const u64 fs = pk2(-hi32(f2[s]), lo32(f2[s]));   // (-fi, fr): operand modifiers
+        acc[s][2 * q] = ffma2(pk2(r.x, r.x), f2[s], acc[s][2 * q]);
+        acc[s][2 * q] = ffma2(fs, pk2(r.y, r.y), acc[s][2 * q]);
+        if (2 * q + 1 < pos) {
+          acc[s][2 * q + 1] = ffma2(pk2(r.z, r.z), f2[s], acc[s][2 * q + 1]);
+          acc[s][2 * q + 1] = ffma2(fs, pk2(r.w, r.w), acc[s][2 * q + 1]);
+        }
       }
     }
   }
@@ -511,11 +552,9 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
     }
     const int64_t gv = c * a.V + v0 + v;
     const float2 z = make_float2((float)(zr - sh[k].x), (float)(zi - sh[k].y));
-    float* zg = reinterpret_cast<float*>(a.zq + gv * NPP) + 4 * (k >> 1) + (k & 1);
-    zg[0] = z.x;
-    zg[2] = z.y;
+    reinterpret_cast<float2*>(a.zq + gv * NPP)[k] = z;   // (re, im) per row
     const float e = row_bound((float)sqrt(yn) * 1.0001f, z, ly[k], k, m, N, L, a.guard_scale, 0);
-    a.thrg[gv * N + k] = 0.5f - e / ly[k].y - MPNL_U * 2.f * L;
+    a.thrg[gv * ((N + 3) & ~3) + k] = 0.5f - e / ly[k].y - MPNL_U * 2.f * L;
     e2s[v * N + k] = (double)e * e;
     zns[v * N + k] = zr * zr + zi * zi;
   }
@@ -578,7 +617,7 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
   for (int q = 0; q < XM; ++q) {
     const int j = N - 1 - q;
     if (j != pos) continue;
-    float ar_ = zrow[4 * (j >> 1) + (j & 1)], ai_ = zrow[4 * (j >> 1) + 2 + (j & 1)];
+    float ar_ = zrow[2 * j], ai_ = zrow[2 * j + 1];
 #pragma unroll
     for (int q2 = 0; q2 < q; ++q2) {
       const int l = N - 1 - q2;
@@ -590,10 +629,10 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
   }
   const float4 lyp = T.lay4[pos];
   // index-domain centre error bound (prep kernel) for the cut guard
-  const float E = 0.5f - a.thrg[gv * N + pos];
+  const float E = 0.5f - a.thrg[gv * ((N + 3) & ~3) + pos];
   // centre in level-index units (unclamped)
-  const float cx = __fmul_rn(__fmul_rn(xr, lyp.x), (float)(L - 1));
-  const float cy = __fmul_rn(__fmul_rn(xi, lyp.x), (float)(L - 1));
+  const float cx = __fmul_rn(xr, lyp.x);
+  const float cy = __fmul_rn(xi, lyp.x);
   // per-axis closest-first level orders in a transposed per-thread scratch
   const int nth = blockDim.x;
   float* scr = scratch + threadIdx.x;
@@ -651,179 +690,248 @@ select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
 
 // ===========================================================================
 // K3: traversal (hot kernel)
+//
+// Persistent CTAs: the grid is sized to the resident capacity and CTA b owns
+// the contiguous item range [b I / G, (b+1) I / G) (MPNL is fixed-complexity,
+// so static ranges are balanced).  An item is one vector (or, when P < 32 PT,
+// `vpi` vectors of the same channel).  The range is walked channel segment by
+// channel segment: the channel's tables are staged in shared memory once per
+// segment, and each warp walks its items with the next item's z' rows, guard
+// thresholds, E_acc and selection lists prefetched by cp.async into a
+// per-warp double buffer, so the global latency hides behind the traversal.
 // ===========================================================================
 struct TravSmem {
-  int tpo, tab, wz, wthr, weac, wy, ev, evn, ylist, lists, total_bytes;
-  __host__ __device__ TravSmem(int m, int n, int warps, int vc, int list_bytes) {
+  int tpo, tab, wbuf, bufsz, zs, thr, eac, lst, xs, ev, evn, total_bytes;   // floats / bytes
+  __host__ __device__ TravSmem(int m, int n, int warps, int nvi, int list_bytes) {
     TableLayout tl(m, n);
+    const int npp = (n + 1) / 2, n4 = (n + 3) & ~3;
+    // per-warp buffer (floats): z' row pairs | thresholds | (E_acc, corr) | lists
+    zs = 0;
+    thr = zs + 4 * nvi * npp;
+    eac = thr + nvi * n4;
+    lst = eac + TableLayout::up4(2 * nvi);
+    bufsz = lst + nvi * list_bytes / 4;
     int o = 0;
     tpo = o; o += TableLayout::up4((int)(sizeof(TreeParams) / 4));
     tab = o; o += tl.total;
-    wz = o; o += warps * 4 * MPNL_VPI_MAX * ((n + 1) / 2);   // per warp z' (VPI x NPP float4)
-    wthr = o; o += warps * MPNL_VPI_MAX * n;       // per warp thresholds
-    weac = o; o += warps * MPNL_VPI_MAX;           // per warp E_acc per vector
-    wy = o; o += 0;                                // (unused)
+    wbuf = o; o += warps * 2 * bufsz;
+    xs = o; o += 2 * MPNL_XMAX * MPNL_PT_SMALL * MPNL_XS_STRIDE;   // u64 per-thread symbols
     ev = o; o += 4 * TRAV_EV_CAP;                  // int4 event buffer
     evn = o; o += 4;
-    ylist = o; o += 0;
-    lists = o * 4;                                 // the chunk's selection lists (bytes)
-    total_bytes = lists + ((vc * list_bytes + 15) & ~15);
+    total_bytes = o * 4;
   }
 };
 
-template <int N, int L>
+// prefetch item (vectors gv0 .. gv0+nv-1) into the warp buffer `buf`
+template <int N>
+__device__ __forceinline__ void trav_prefetch(const DetectArgs& a, const TravSmem& so, float* buf,
+                                              int gv0, int nv, int list_bytes, int lane) {
+  constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
+  const float4* zsrc = a.zq + (int64_t)gv0 * NPP;
+  for (int i = lane; i < nv * NPP; i += 32) cp_async16(buf + so.zs + 4 * i, zsrc + i);
+  const float* tsrc = a.thrg + (int64_t)gv0 * N4;
+  for (int i = lane; i < nv * (N4 / 4); i += 32) cp_async16(buf + so.thr + 4 * i, tsrc + 4 * i);
+  if (lane < nv) cp_async8(buf + so.eac + 2 * lane, a.vaux + gv0 + lane);
+  if (list_bytes) {
+    const uint8_t* lsrc = a.lists + (int64_t)gv0 * list_bytes;
+    for (int i = lane; i < nv * (list_bytes >> 4); i += 32)
+      cp_async16(buf + so.lst + 4 * i, lsrc + 16 * i);
+  }
+  cp_async_commit();
+}
+
+// VPI = false: one vector per item, its P paths in bpv batches of 32 PT paths
+//              (every path of a lane is on the same vector);
+// VPI = true : vpi = 32 PT / P vectors per item, one batch.
+template <int N, int L, bool VPI>
 __global__ void __launch_bounds__(TravCfg<N>::MAXT, TravCfg<N>::MINB)
 traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   constexpr int PT = TravCfg<N>::PT;
   constexpr int S = 32 * PT;
   extern __shared__ __align__(16) float sm[];
   const int nth = blockDim.x, nw = nth >> 5;
-  const TravSmem so(a.m, N, nw, a.vc, tparam.list_bytes);
+  const int nvi = VPI ? a.vpi : 1;                          // vectors per item
+  const TravSmem so(a.m, N, nw, nvi, tparam.list_bytes);
   const TableLayout tl(a.m, N);
-  const int m = a.m;
-  const int64_t c = blockIdx.x / a.chunks;
-  const int v0 = (blockIdx.x % a.chunks) * a.vc;
-  const int vce = (int)min((int64_t)a.vc, a.V - v0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const float INF = __int_as_float(0x7f800000);
   TreeParams& tp = *reinterpret_cast<TreeParams*>(sm + so.tpo);
   float* tab = sm + so.tab;
-  constexpr int NPP = (N + 1) / 2;
-  float4* zs = reinterpret_cast<float4*>(sm + so.wz) + warp * MPNL_VPI_MAX * NPP;
-  float* thr = sm + so.wthr + warp * MPNL_VPI_MAX * N;
-  float* weacc = sm + so.weac + warp * MPNL_VPI_MAX;
-  uint8_t* lch = reinterpret_cast<uint8_t*>(sm) + so.lists;
+  float* wb0 = sm + so.wbuf + warp * 2 * so.bufsz;
   int4* evb = reinterpret_cast<int4*>(sm + so.ev);
   int* evn = reinterpret_cast<int*>(sm + so.evn);
   {
     const int* s = reinterpret_cast<const int*>(&tparam);
     int* d = reinterpret_cast<int*>(&tp);
     for (int i = tid; i < (int)(sizeof(TreeParams) / 4); i += nth) d[i] = s[i];
-    const float4* src = reinterpret_cast<const float4*>(a.tables + c * (int64_t)tl.total);
-    float4* dst = reinterpret_cast<float4*>(tab);
-    for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
     if (tid == 0) { evn[0] = 0; evn[1] = 0; }
-    // the chunk's partial-layer lists (contiguous in global)
-    const int64_t g0 = c * a.V + v0;
-    const int lb = tparam.list_bytes;
-    if (lb) {
-      const uint8_t* lsrc = a.lists + g0 * lb;
-      if ((lb & 3) == 0) {
-        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(lsrc);
-        uint32_t* d4 = reinterpret_cast<uint32_t*>(lch);
-        for (int i = tid; i < vce * lb / 4; i += nth) d4[i] = s4[i];
-      } else {
-        for (int i = tid; i < vce * lb; i += nth) lch[i] = lsrc[i];
+  }
+  const int P = tparam.n_paths;
+  const int lbytes = tparam.list_bytes;
+  const int bpv = VPI ? 1 : a.bpv;
+  // paths are fixed per lane when one batch covers them: precompute the
+  // expanded layers' symbols (float pair) / list indices once
+  u64* xs = reinterpret_cast<u64*>(sm + so.xs) + tid;
+  const bool use_xs = bpv == 1;
+  if (use_xs) {
+    constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {
+      const int s = t * 32 + lane;
+      const int p = VPI ? s % P : s;
+#pragma unroll
+      for (int j = 0; j < XM; ++j) {
+        const int pos = N - 1 - j;
+        u64 x = 0ull;
+        if (j < tparam.n_top && p < P) {
+          const int e = tparam.e[pos];
+          const int d = p / tparam.stride[pos];
+          if (e == L * L) {
+            const int dd = d % e;
+            x = pk2((float)(dd / L), (float)(dd % L));
+          } else {
+            x = (u64)(unsigned)(tparam.list_off[pos] + d);
+          }
+        }
+        xs[(j * PT + t) * MPNL_XS_STRIDE] = x;
       }
     }
   }
-  __syncthreads();
-  const TabPtrs T = tab_ptrs(tab, m, N);
-  const int P = tp.n_paths;
-  const bool batch = a.bpv > 1 || a.vpi == 1;
-  const int nvi = batch ? 1 : a.vpi;                       // vectors per item
-  const int items = (vce + nvi - 1) / nvi;
-  const int64_t gbase = c * a.V + v0;
+  const int V = (int)a.V;
+  const int ipc = (V + nvi - 1) / nvi;                      // items per channel
+  const int64_t I = a.n_ch * (int64_t)ipc;
+  const int it_begin = (int)((int64_t)blockIdx.x * I / gridDim.x);
+  const int it_end = (int)((int64_t)(blockIdx.x + 1) * I / gridDim.x);
+  const TabPtrs T = tab_ptrs(tab, a.m, N);
 
-  for (int item = warp; item < items; item += nw) {
-    // ---- prologue: the item's z' rows, guard thresholds, E_acc (prep kernel) ----
-#pragma unroll 1
-    for (int j = 0; j < nvi; ++j) {
-      const int vl = item * nvi + j;
-      if (vl >= vce) break;
-      const int64_t gv = gbase + vl;
-      if (lane < NPP) zs[j * NPP + lane] = a.zq[gv * NPP + lane];
-      if (lane < N) thr[j * N + lane] = a.thrg[gv * N + lane];
-      if (lane == 0) weacc[j] = a.vaux[gv].x;
+  for (int seg = it_begin; seg < it_end;) {
+    const int c = seg / ipc;
+    const int ibase = c * ipc, vbase = c * V;
+    const int seg_end = min(it_end, ibase + ipc);
+    __syncthreads();   // previous segment's tables no longer in use (and xs / tp ready)
+    {
+      const float4* src = reinterpret_cast<const float4*>(a.tables + (int64_t)c * tl.total);
+      float4* dst = reinterpret_cast<float4*>(tab);
+      for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
     }
-    __syncwarp();
-    // ---- traversal over path batches ----
-    Top3 run = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
-    float wb = INF;   // warp-wide best so far of this vector (batch mode)
-    for (int b = 0; b < a.bpv; ++b) {
-      int vl[PT], pp[PT];
-      int64_t gvl[PT];
-      bool ok[PT];
-#pragma unroll
-      for (int t = 0; t < PT; ++t) {
-        const int s = t * 32 + lane;
-        if (batch) {
-          vl[t] = 0;
-          pp[t] = b * S + s;
-          ok[t] = pp[t] < P;
-        } else {
-          vl[t] = s / P;
-          pp[t] = s % P;
-          ok[t] = vl[t] < nvi && item * nvi + vl[t] < vce;
-        }
-        if (!ok[t]) { vl[t] = 0; pp[t] = 0; }
-        gvl[t] = item * nvi + vl[t];   // chunk-local vector (lists staged in smem)
-      }
-      float ped[PT], evp[PT];
-      unsigned evm[PT];
-      traverse_paths<N, L, PT, true, false>(T, zs, thr, lch, tp, tp.list_bytes, vl, gvl, pp, ped,
-                                            evm, evp);
-      // log paths with a marked decision whose prefix may still be competitive
-      const float bnd = (wb == INF) ? INF : wb + 2.f * ped_tol(wb, weacc[0], N);
-#pragma unroll
-      for (int t = 0; t < PT; ++t) {
-        if (ok[t] && evm[t] != 0u && evp[t] <= bnd) {
-          const int4 e4 = make_int4(pp[t], (int)evm[t], (int)(gbase + gvl[t]), EV_NODE);
-          const int idx = atomicAdd(evn, 1);
-          if (idx < TRAV_EV_CAP) evb[idx] = e4;
-          else log_event(a, e4);
-        }
-      }
-      if (batch) {
-#pragma unroll
-        for (int t = 0; t < PT; ++t)
-          if (ok[t]) top3_insert(run, ped[t], (unsigned)pp[t]);
-        wb = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
-      } else if (P >= 32) {
-        const int g = P >> 5;   // t-slots per vector
-#pragma unroll
-        for (int t0 = 0; t0 < PT; ++t0) {
-          if (t0 % g) continue;
-          Top3 x = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
-#pragma unroll
-          for (int t = 0; t < PT; ++t)
-            if (t >= t0 && t < t0 + g && ok[t]) top3_insert(x, ped[t], (unsigned)pp[t]);
-          float b1, b2, b3;
-          unsigned q1, q2;
-          warp_top3(x, b1, q1, b2, q2, b3);
-          const int j = t0 / g;
-          const int vlj = item * nvi + j;
-          if (lane == 0 && j < nvi && vlj < vce) {
-            a.vres[gbase + vlj] = make_float4(b1, b2, b3, weacc[j]);
-            a.vpath[gbase + vlj] = make_int2((int)q1, (int)q2);
-          }
-        }
+    __syncthreads();
+    int k = 0;
+    int it = seg + warp;
+    if (it < seg_end) {
+      const int j = (it - ibase) * nvi;
+      trav_prefetch<N>(a, so, wb0, vbase + j, min(nvi, V - j), lbytes, lane);
+    }
+    for (; it < seg_end; it += nw, k ^= 1) {
+      const int nxt = it + nw;
+      if (nxt < seg_end) {
+        const int j = (nxt - ibase) * nvi;
+        trav_prefetch<N>(a, so, wb0 + (k ^ 1) * so.bufsz, vbase + j, min(nvi, V - j), lbytes,
+                         lane);
+        cp_async_wait<1>();
       } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const float* buf = wb0 + k * so.bufsz;
+      const float4* zs = reinterpret_cast<const float4*>(buf + so.zs);
+      const float* thr = buf + so.thr;
+      const float* weacc = buf + so.eac;                    // (E_acc, corr) pairs
+      const uint8_t* lch = reinterpret_cast<const uint8_t*>(buf + so.lst);
+      const int jv = (it - ibase) * nvi;
+      const int gbase = vbase + jv;
+      const int vce = min(nvi, V - jv);
+
+      Top3 run = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
+      float wbest = INF;   // warp-wide best so far of this vector (multi-batch)
+      for (int b = 0; b < bpv; ++b) {
+        int vl[PT], pp[PT];
+        int64_t gvl[PT];
+        bool ok[PT];
 #pragma unroll
         for (int t = 0; t < PT; ++t) {
-          Top3 x = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
-          if (ok[t]) top3_insert(x, ped[t], (unsigned)pp[t]);
-          float b1, b2, b3;
-          unsigned q1, q2;
-          group_top3(x, P, b1, q1, b2, q2, b3);
-          const int j = (t * 32 + lane) / P;
-          const int vlj = item * nvi + j;
-          if ((lane % P) == 0 && j < nvi && vlj < vce) {
-            a.vres[gbase + vlj] = make_float4(b1, b2, b3, weacc[j]);
-            a.vpath[gbase + vlj] = make_int2((int)q1, (int)q2);
+          const int s = t * 32 + lane;
+          if (!VPI) {
+            vl[t] = 0;
+            pp[t] = b * S + s;
+            ok[t] = pp[t] < P;
+          } else {
+            vl[t] = s / P;
+            pp[t] = s % P;
+            ok[t] = vl[t] < vce;
+          }
+          if (!ok[t]) { vl[t] = 0; pp[t] = 0; }
+          gvl[t] = vl[t];   // lists of the item's vectors in the warp buffer
+        }
+        float ped[PT], evp[PT];
+        unsigned evm[PT];
+        traverse_paths<N, L, PT, true, false, !VPI>(T, zs, thr, lch, tp, lbytes, vl, gvl, pp, ped,
+                                                    evm, evp, nullptr, nullptr, -1,
+                                                    use_xs ? xs : nullptr);
+        // log paths with a marked decision whose prefix may still be competitive
+#pragma unroll
+        for (int t = 0; t < PT; ++t) {
+          if (ok[t] && evm[t] != 0u) {
+            const float bnd = (wbest == INF) ? INF : wbest + 2.f * ped_tol(wbest, weacc[0], N);
+            if (evp[t] <= bnd) {
+              const int4 e4 = make_int4(pp[t], (int)evm[t], gbase + vl[t], EV_NODE);
+              const int idx = atomicAdd(evn, 1);
+              if (idx < TRAV_EV_CAP) evb[idx] = e4;
+              else log_event(a, e4);
+            }
+          }
+        }
+        if (!VPI) {
+#pragma unroll
+          for (int t = 0; t < PT; ++t)
+            if (ok[t]) top3_insert(run, ped[t], (unsigned)pp[t]);
+          if (bpv > 1)
+            wbest = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
+        } else if (P >= 32) {
+          const int g = P >> 5;   // t-slots per vector
+#pragma unroll
+          for (int t0 = 0; t0 < PT; ++t0) {
+            if (t0 % g) continue;
+            Top3 x = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
+#pragma unroll
+            for (int t = 0; t < PT; ++t)
+              if (t >= t0 && t < t0 + g && ok[t]) top3_insert(x, ped[t], (unsigned)pp[t]);
+            float b1, b2, b3;
+            unsigned q1, q2;
+            warp_top3(x, b1, q1, b2, q2, b3);
+            const int j = t0 / g;
+            if (lane == 0 && j < vce) {
+              a.vres[gbase + j] = make_float4(b1, b2, b3, weacc[2 * j]);
+              a.vpath[gbase + j] = make_int2((int)q1, (int)q2);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < PT; ++t) {
+            Top3 x = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
+            if (ok[t]) top3_insert(x, ped[t], (unsigned)pp[t]);
+            float b1, b2, b3;
+            unsigned q1, q2;
+            group_top3(x, P, b1, q1, b2, q2, b3);
+            const int j = (t * 32 + lane) / P;
+            if ((lane % P) == 0 && j < vce) {
+              a.vres[gbase + j] = make_float4(b1, b2, b3, weacc[2 * j]);
+              a.vpath[gbase + j] = make_int2((int)q1, (int)q2);
+            }
           }
         }
       }
-    }
-    if (batch) {
-      float b1, b2, b3;
-      unsigned q1, q2;
-      warp_top3(run, b1, q1, b2, q2, b3);
-      if (lane == 0) {
-        a.vres[gbase + item] = make_float4(b1, b2, b3, weacc[0]);
-        a.vpath[gbase + item] = make_int2((int)q1, (int)q2);
+      if (!VPI) {
+        float b1, b2, b3;
+        unsigned q1, q2;
+        warp_top3(run, b1, q1, b2, q2, b3);
+        if (lane == 0) {
+          a.vres[gbase] = make_float4(b1, b2, b3, weacc[0]);
+          a.vpath[gbase] = make_int2((int)q1, (int)q2);
+        }
       }
+      __syncwarp();   // the buffer is refilled by the prefetch two items ahead
     }
+    seg = seg_end;
   }
   // ---- flush the CTA's event buffer to the global log ----
   __syncthreads();
@@ -910,9 +1018,9 @@ __device__ __forceinline__ void warp_retrace(const float* tab, int m, const floa
   const TabPtrs T = tab_ptrs(tab, m, N);
   float ar = 0.f, ai = 0.f;
   if (lane < N) {
-    const float* zf = reinterpret_cast<const float*>(zrow + (lane >> 1));
-    ar = zf[lane & 1];
-    ai = zf[2 + (lane & 1)];
+    const float2 zf = reinterpret_cast<const float2*>(zrow)[lane];
+    ar = zf.x;
+    ai = zf.y;
   }
   u64 ped2 = 0ull;
   const int top_lo = N - tp.n_top;

@@ -3,6 +3,8 @@
 // launcher the C ABI dispatches to.  Included by the traverse_l<L>_p<part>.cu
 // units (one per constellation x N-range, compiled in parallel).
 #pragma once
+#include <algorithm>
+
 #include "traverse.cuh"
 
 namespace mpnl {
@@ -15,8 +17,16 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
   if (kind == 0) {
     select_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
   } else if (kind == 1) {
-    auto k = traverse_kernel<NN, L>;
+    // persistent: grid = resident capacity (capped by the item count `extra`)
+    auto k = a.vpi > 1 ? traverse_kernel<NN, L, true> : traverse_kernel<NN, L, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (grid == 0) {
+      int nb = 0, dev = 0, sms = 148;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, threads, smem);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      grid = (unsigned)std::min<long long>((long long)std::max(nb, 1) * sms, (long long)extra);
+    }
     k<<<grid, threads, smem, st>>>(a, tp);
   } else if (kind == 4) {
     auto k = prep_kernel<NN, L>;

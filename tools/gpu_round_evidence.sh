@@ -19,4 +19,8 @@ for c in C1 C2 C3 C4 C5P16 C5P64 C5P256 C5P1024; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:traverse_kernel -c 1 -o $O/${TAG}_trav_$c \
     python tools/profile_one.py $c 0 1 > $O/${TAG}_ncu_$c.log 2>&1; echo ncu_$c rc=$?
 done
+python tools/ncu_summary.py traffic $TAG $O/profiles_$TAG > /dev/null; echo traffic_rc=$?
+python tools/ncu_summary.py launches $O/${TAG}_launches_default.csv > $O/profiles_$TAG/${TAG}_launches_default.txt
+for c in C1 C3 C4 C5P16 C5P64 C5P256 C5P1024; do rm -f $O/${TAG}_trav_$c.ncu-rep; done
+du -sh $O
 cat $O/${TAG}_bench_default.json $O/${TAG}_bench_reference.json

@@ -66,8 +66,8 @@ def _bytes(v, unit):
                                         "Gbyte": 1e9}.get(unit, 1)
 
 
-def traffic(tag):
-    """profiles/traffic.json from gpurun_out/<tag>_trav_<cfg>.ncu-rep captures."""
+def traffic(tag, outdir="profiles"):
+    """<outdir>/traffic.json from gpurun_out/<tag>_trav_<cfg>.ncu-rep captures."""
     import glob
     import json
     import os
@@ -81,8 +81,8 @@ def traffic(tag):
         res[cfg] = {"dram_bytes_per_launch": int(rd + wr), "read": int(rd), "write": int(wr),
                     "kernel": d["Kernel Name"].split("(")[0],
                     "source": f"profiles/{tag}_ncu_traverse_{cfg}.txt (ncu --set full)"}
-        os.makedirs("profiles", exist_ok=True)
-        with open(f"profiles/{tag}_ncu_traverse_{cfg}.txt", "w") as f:
+        os.makedirs(outdir, exist_ok=True)
+        with open(f"{outdir}/{tag}_ncu_traverse_{cfg}.txt", "w") as f:
             import contextlib
             import io
             buf = io.StringIO()
@@ -90,7 +90,7 @@ def traffic(tag):
                 full(p)
             f.write(f"# ncu --set full --clock-control none, {cfg} full size, from {os.path.basename(p)}\n")
             f.write(buf.getvalue())
-    with open("profiles/traffic.json", "w") as f:
+    with open(f"{outdir}/traffic.json", "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1))
 
@@ -109,7 +109,8 @@ def launches(path):
             k = d["Kernel Name"].split("(")[0][:70]
             v = float(d["Metric Value"].replace(",", ""))
             unit = d["Metric Unit"]
-            v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+                  "ms": 1e3}.get(unit, 1.0)
             tot[k] += v
             cnt[k] += 1
     s = sum(tot.values()) or 1.0
@@ -119,4 +120,4 @@ def launches(path):
 
 
 if __name__ == "__main__":
-    {"full": full, "launches": launches, "traffic": traffic}[sys.argv[1]](sys.argv[2])
+    {"full": full, "launches": launches, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
