@@ -101,7 +101,7 @@ int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64,
  * the rigorous bound; <= 0 restores the default).  Diagnostics only. */
 void mpnl_set_guard_scale(double c);
 
-/* Optional device int32[8] counters (NULL disables; diagnostics only):
+/* Optional device int32[8] counters (NULL disables; diagnostics only): [0] events logged,
  * [1] guarded decisions re-decided in fp64, [2] two-way near-ties settled in
  * fp64, [3] vectors sent to the fp64 kernel, of which [4] three-way ties,
  * [5] fp64-level ties, [6] fp64 disagreements, [7] event-log overflows. */
@@ -110,6 +110,9 @@ void mpnl_set_stats(int32_t* device_counters);
 /* FFMA throughput probe (for the roofline denominator): runs `iters` dependent
  * FFMA chains on every SM; returns FLOPs executed.  out: device float[blocks*threads]. */
 int64_t mpnl_ffma_probe(float* out, int blocks, int threads, int iters, void* stream);
+
+/* Same for the packed fma.rn.f32x2 (FFMA2) instruction the traversal uses. */
+int64_t mpnl_ffma2_probe(float* out, int blocks, int threads, int iters, void* stream);
 
 #ifdef __cplusplus
 }

@@ -8,10 +8,12 @@ machine has no CUDA device, every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libmpnl_b200.so"
+_LIB_PATH = Path(os.environ.get("MPNL_LIB") or
+                 Path(__file__).resolve().parent / "_lib" / "libmpnl_b200.so")
 _lock = threading.Lock()
 _lib = None
 
@@ -34,6 +36,7 @@ _SIGS = {
     "mpnl_set_guard_scale": ([_f64], None),
     "mpnl_set_stats": ([_vp], None),
     "mpnl_ffma_probe": ([_vp, _i32, _i32, _i32, _vp], _i64),
+    "mpnl_ffma2_probe": ([_vp, _i32, _i32, _i32, _vp], _i64),
 }
 
 

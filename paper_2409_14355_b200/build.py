@@ -17,12 +17,15 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
+# MPNL_VARIANT=<name> MPNL_EXTRA_FLAGS="-D..." builds an experimental variant
+# into _lib/libmpnl_b200_<name>.so (load it with MPNL_LIB=<path>)
+_VARIANT = os.environ.get("MPNL_VARIANT", "")
 OUT_DIR = PKG / "_lib"
-LIB = OUT_DIR / "libmpnl_b200.so"
-OBJ_DIR = PKG.parent / "build" / "obj"
+LIB = OUT_DIR / (f"libmpnl_b200_{_VARIANT}.so" if _VARIANT else "libmpnl_b200.so")
+OBJ_DIR = PKG.parent / "build" / (f"obj_{_VARIANT}" if _VARIANT else "obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                     "-I", str(PKG.parent / "include")]
+                     "-I", str(PKG.parent / "include")] + os.environ.get("MPNL_EXTRA_FLAGS", "").split()
 
 
 def _nvcc() -> str:

@@ -318,14 +318,17 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
       const int64_t pch = (v_per_ch + PREP_VC - 1) / PREP_VC;
       if (n_ch * pch > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
       const PrepSmem ps(m, n);
-      e = launch_fast(n, L, 4, a, tp, (unsigned)(n_ch * pch), 128, ps.total, (int)pch, st);
+      e = launch_fast(n, L, 4, a, tp, (unsigned)(n_ch * pch), PrepSmem::threads(n), ps.total,
+                      (int)pch, st);
     }
     if (e != cudaSuccess) return cuda_fail(e, "prep kernel");
     for (int pos = n - 1; pos >= n - tp.n_top; --pos) {
       if (tp.e[pos] == L * L) continue;
-      const int64_t items = B * (tp.n_paths / tp.stride[pos + 1]);
-      if (items > 0x7fffffffLL * 128) return fail(MPNL_EUNSUPPORTED, "selection grid too large");
-      e = launch_fast(n, L, 0, a, tp, (unsigned)((items + 127) / 128), 128, 0, pos, st);
+      const int npar = tp.n_paths / tp.stride[pos + 1];
+      const int px = std::min(npar, 128), vy = std::max(1, 128 / px);
+      if ((B + vy - 1) / vy > 0x7fffffffLL || (npar + px - 1) / px > 65535)
+        return fail(MPNL_EUNSUPPORTED, "selection grid too large");
+      e = launch_fast(n, L, 0, a, tp, 0, 128, 0, pos, st);
       if (e != cudaSuccess) return cuda_fail(e, "select kernel");
     }
     return MPNL_OK;
@@ -383,7 +386,7 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   } else {
     ea.list = a.fix_list;
     ea.count = a.counters;
-    grid = 148 * 8;
+    grid = 148 * 2;   // a handful of flagged vectors: few, long-lived CTAs
   }
   e = launch_exact(ea, tp, grid, st);
   if (e != cudaSuccess) return cuda_fail(e, "exact kernel");
@@ -456,6 +459,40 @@ __global__ void ffma_probe_kernel(float* out, int iters) {
     x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+// packed FFMA2 throughput (the instruction the traversal is built on):
+// 8 independent f32x2 accumulators, a register pair and a broadcast operand
+__global__ void ffma2_probe_kernel(float* out, int iters) {
+  typedef unsigned long long u64;
+  auto pk = [](float lo, float hi) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+  };
+  auto fma2 = [](u64 a, u64 b, u64 c) {
+    u64 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+  };
+  const float t = threadIdx.x * 1e-3f;
+  const u64 x = pk(0.999999f + t * 1e-9f, 0.999998f), b = pk(1e-7f, 1e-7f);
+  u64 a0 = pk(t, t + 1.f), a1 = pk(t + 2.f, t + 3.f), a2 = pk(t + 4.f, t + 5.f),
+      a3 = pk(t + 6.f, t + 7.f), a4 = pk(t + 8.f, t + 9.f), a5 = pk(t + 10.f, t + 11.f),
+      a6 = pk(t + 12.f, t + 13.f), a7 = pk(t + 14.f, t + 15.f);
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma2(a0, x, b); a1 = fma2(a1, x, b); a2 = fma2(a2, x, b); a3 = fma2(a3, x, b);
+    a4 = fma2(a4, x, b); a5 = fma2(a5, x, b); a6 = fma2(a6, x, b); a7 = fma2(a7, x, b);
+  }
+  const u64 s = a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __uint_as_float((unsigned)s);
+}
+
+extern "C" int64_t mpnl_ffma2_probe(float* out, int blocks, int threads, int iters, void* stream) {
+  ffma2_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(out, iters);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  return (int64_t)blocks * threads * iters * 8 * 2 * 2;
 }
 
 extern "C" int64_t mpnl_ffma_probe(float* out, int blocks, int threads, int iters, void* stream) {

@@ -1,301 +1,30 @@
-// K5 — fp64 parallel-path detector with the reference's exact decision rules.
-//
-// Two uses:
-//   * fix-up of the vectors the fp32 path could not certify (three-way
-//     near-ties, fp64-level ties, a guarded decision whose fp64 branch could
-//     win): recomputed here, results overwritten;
-//   * the reference-compatible full candidate list of `mpnl_detect_batch`
-//     (`/root/reference/pkg/src/mpnlsim/detect.py:473-488`): labels (B,P,N) in
-//     path order, metrics (B,P), best (B,);
-//   * overloaded channels (N > M, augmented planning) and trees with more than
-//     three expanded layers.
-//
-// Semantics followed (detect.py):
-//   centre = (z_pos - acc_pos) / Re r_pp                         :417
-//   children = stable argsort(|centre - s_q|^2)[:e]              :418-419
-//     (ties -> lower point label; e = 1 is the 2-D nearest point, found
-//      per axis for square QAM with the same tie rule)
-//   path index mixed radix, top layer most significant           :420-422
-//   metric: true residual; computed here as the fp64 PED plus
-//     ||y||^2 - ||z||^2 (M > N) minus nv ||x||^2 (augmented)      :484-486
-//   best = lexicographic (metric, labels[stream 0], labels[1], ...) :465-470
-//
-// One CTA per received vector (grid-stride over the task list):
-//   1. z = Q^H y in fp64 (thread per row);
-//   2. selection lists of the expanded layers, top-down, thread per
-//      (parent, point): rank of the point among the parent's Q children by
-//      (distance, label) — an O(Q) count, no per-path sorting;
-//   3. thread per path: fp64 SIC below the listed prefix;
-//   4. block tree-argmin on (metric, labels).
-#include <math_constants.h>
-
+// Host dispatch of the fp64 exact kernel (exact.cuh), instantiated per
+// (N, L) in the traverse_l<L>_p<part>.cu units.
 #include "exact_args.cuh"
-#include "fp64dec.cuh"
 
 namespace mpnl {
 
-#define EX_THREADS 256
-#define EX_LIST_MAX (48 * 1024)
-
-struct ExLayout {   // dynamic shared memory (bytes)
-  int tp, z, misc, cand_m, cand_p, cand_l, lists, total;
-  int list_off[MPNL_MAX_N];
-  bool listed[MPNL_MAX_N];
-  int list_bytes;
-  __host__ __device__ ExLayout(const TreeParams& t, int n, int L, int exact_order) {
-    int lb = 0;
-    for (int pos = n - 1; pos >= 0; --pos) {
-      const int e = t.e[pos];
-      listed[pos] = e > 1 && (e < L * L || exact_order);
-      list_off[pos] = lb;
-      if (listed[pos]) lb += t.n_paths / t.stride[pos];
-    }
-    list_bytes = lb;
-    int o = 0;
-    tp = o; o += (int)sizeof(TreeParams);
-    o = (o + 15) & ~15;
-    z = o; o += 16 * MPNL_MAX_N;
-    misc = o; o += 32;
-    cand_m = o; o += 8 * EX_THREADS;
-    cand_p = o; o += 4 * EX_THREADS;
-    cand_l = o; o += MPNL_MAX_N * EX_THREADS;
-    lists = o; o += (lb <= EX_LIST_MAX ? lb : 0);
-    total = (o + 15) & ~15;
-  }
-};
-
-__device__ __forceinline__ bool ex_better(double m1, const uint8_t* l1, double m2,
-                                          const uint8_t* l2, int n) {
-  if (m1 != m2) return m1 < m2;
-  for (int i = 0; i < n; ++i)
-    if (l1[i] != l2[i]) return l1[i] < l2[i];
-  return false;
-}
-
-__global__ void __launch_bounds__(EX_THREADS)
-exact_kernel(const ExactArgs a, const TreeParams tparam) {
-  extern __shared__ __align__(16) uint8_t exsm[];
-  const int n = a.n, m = a.m, L = a.L, Q = L * L;
-  const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
-  const double nrm = qam_norm_d(L);
-  const ExLayout lo(tparam, n, L, a.exact_order);
-  TreeParams& tp = *reinterpret_cast<TreeParams*>(exsm + lo.tp);
-  double2* zs = reinterpret_cast<double2*>(exsm + lo.z);
-  double* misc = reinterpret_cast<double*>(exsm + lo.misc);
-  double* cm = reinterpret_cast<double*>(exsm + lo.cand_m);
-  int* cp = reinterpret_cast<int*>(exsm + lo.cand_p);
-  uint8_t* cl = exsm + lo.cand_l;
-  uint8_t* lists = exsm + lo.lists;
-  const bool use_lists = lo.list_bytes <= EX_LIST_MAX;
-  const int tid = threadIdx.x;
-  {
-    const int* s = reinterpret_cast<const int*>(&tparam);
-    int* d = reinterpret_cast<int*>(&tp);
-    for (int i = tid; i < (int)(sizeof(TreeParams) / 4); i += EX_THREADS) d[i] = s[i];
-  }
-  __syncthreads();
-  const int64_t ntask = a.list ? (int64_t)(*a.count) : a.n_tasks;
-  const int P = tp.n_paths;
-  for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
-    const int64_t gv = a.list ? a.list[task] : task;
-    const int64_t c = gv / a.V;
-    const double2* R = a.r64 + c * (int64_t)n * n;
-    const double2* QH = a.qh64 + c * (int64_t)n * m;
-    const int32_t* pc = a.perm + c * n;
-    auto yat = [&](int r, double& yr, double& yi) {
-      if (a.y_f64) {
-        const double2 v = reinterpret_cast<const double2*>(a.y)[gv * m + r];
-        yr = v.x; yi = v.y;
-      } else {
-        const float2 v = reinterpret_cast<const float2*>(a.y)[gv * m + r];
-        yr = v.x; yi = v.y;
-      }
-    };
-    // ---- 1. z = Q^H y ; c0 = ||y||^2 - ||z||^2 (M != N) ----
-    if (tid < n) {
-      double zr = 0.0, zi = 0.0;
-      for (int r = 0; r < m; ++r) {
-        double yr, yi;
-        yat(r, yr, yi);
-        const double2 q = QH[tid * m + r];
-        zr = fma(q.x, yr, fma(-q.y, yi, zr));
-        zi = fma(q.x, yi, fma(q.y, yr, zi));
-      }
-      zs[tid] = make_double2(zr, zi);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double yn = 0.0, zn = 0.0;
-      for (int r = 0; r < m; ++r) {
-        double yr, yi;
-        yat(r, yr, yi);
-        yn = fma(yr, yr, fma(yi, yi, yn));
-      }
-      for (int k = 0; k < n; ++k) zn = fma(zs[k].x, zs[k].x, fma(zs[k].y, zs[k].y, zn));
-      misc[0] = (m != n) ? (yn - zn) : 0.0;
-    }
-    // ---- 2. exact selection lists of the expanded layers, top-down ----
-    // symbol of path p at an expanded layer (list or digit)
-    auto sym_at = [&](int pos, int p, int& ir, int& ii) {
-      const int e = tp.e[pos];
-      const int d = (p / tp.stride[pos]) % e;
-      if (use_lists && lo.listed[pos]) {
-        const uint8_t b = lists[lo.list_off[pos] + p / tp.stride[pos]];
-        ir = b >> 3; ii = b & 7;
-      } else {
-        ir = d / L; ii = d % L;   // full layer in hard mode: any bijection
-      }
-    };
-    if (use_lists) {
-      for (int pos = n - 1; pos >= 0 && tp.e[pos] > 1; --pos) {
-        if (!lo.listed[pos]) continue;
-        __syncthreads();
-        const int e = tp.e[pos];
-        const int npar = P / tp.stride[pos + 1];
-        for (int it = tid; it < npar * Q; it += EX_THREADS) {
-          const int par = it / Q, q = it % Q;
-          const int p0 = par * tp.stride[pos + 1];
-          double ur = zs[pos].x, ui = zs[pos].y;
-          for (int j = n - 1; j > pos; --j) {
-            int ir, ii;
-            sym_at(j, p0, ir, ii);
-            const double sr = level_value(ir, L, nrm), si = level_value(ii, L, nrm);
-            const double2 r = R[pos * n + j];
-            ur -= r.x * sr - r.y * si;
-            ui -= r.x * si + r.y * sr;
-          }
-          const double rpp = R[pos * n + pos].x;
-          const double cr = ur / rpp, ci = ui / rpp;
-          auto key = [&](int qq, double& d, int& lb) {
-            const int i = qq / L, j = qq % L;
-            const double dr = cr - level_value(i, L, nrm), di = ci - level_value(j, L, nrm);
-            d = dr * dr + di * di;
-            lb = (gray_code(i) << h) | gray_code(j);
-          };
-          double dq;
-          int lq;
-          key(q, dq, lq);
-          int rank = 0;
-          for (int q2 = 0; q2 < Q; ++q2) {
-            double d2;
-            int l2;
-            key(q2, d2, l2);
-            rank += (d2 < dq) || (d2 == dq && l2 < lq);
-          }
-          if (rank < e) lists[lo.list_off[pos] + par * e + rank] = (uint8_t)(((q / L) << 3) | (q % L));
-        }
-      }
-    }
-    __syncthreads();
-    const double c0 = misc[0];
-    // ---- 3. thread per path ----
-    double bm = CUDART_INF;
-    int bp = 0x7fffffff;
-    uint8_t blab[MPNL_MAX_N];
-    for (int p = tid; p < P; p += EX_THREADS) {
-      double2 acc[MPNL_MAX_N];
-      uint8_t lab[MPNL_MAX_N];
-      for (int k = 0; k < n; ++k) acc[k] = make_double2(0.0, 0.0);
-      double ped = 0.0, xs2 = 0.0;
-      for (int pos = n - 1; pos >= 0; --pos) {
-        const double rpp = R[pos * n + pos].x;
-        const double ur = zs[pos].x - acc[pos].x, ui = zs[pos].y - acc[pos].y;
-        const int e = tp.e[pos];
-        int ir, ii;
-        if (e == 1) {
-          ir = nearest_level_f64(ur / rpp, L, nrm);
-          ii = nearest_level_f64(ui / rpp, L, nrm);
-        } else if (use_lists || !(e < Q || a.exact_order)) {
-          sym_at(pos, p, ir, ii);
-        } else {
-          // (lists too large for shared memory) d-th point in stable order
-          const double cr = ur / rpp, ci = ui / rpp;
-          const int d = (p / tp.stride[pos]) % e;
-          double pd = -1.0;
-          int pl = -1, bq = 0;
-          for (int rnk = 0; rnk <= d; ++rnk) {
-            double bd = CUDART_INF;
-            int bl = 1 << 30;
-            for (int q = 0; q < Q; ++q) {
-              const int i = q / L, j = q % L;
-              const double dr = cr - level_value(i, L, nrm), di = ci - level_value(j, L, nrm);
-              const double dd = dr * dr + di * di;
-              const int lb = (gray_code(i) << h) | gray_code(j);
-              const bool after = dd > pd || (dd == pd && lb > pl);
-              const bool better = dd < bd || (dd == bd && lb < bl);
-              if (after && better) { bd = dd; bl = lb; bq = q; }
-            }
-            pd = bd; pl = bl;
-          }
-          ir = bq / L; ii = bq % L;
-        }
-        const double sr = level_value(ir, L, nrm), si = level_value(ii, L, nrm);
-        const double er = ur - rpp * sr, ei = ui - rpp * si;
-        ped = fma(er, er, fma(ei, ei, ped));
-        xs2 = fma(sr, sr, fma(si, si, xs2));
-        lab[pc[pos]] = (uint8_t)((gray_code(ir) << h) | gray_code(ii));
-        for (int k = 0; k < pos; ++k) {
-          const double2 r = R[k * n + pos];
-          acc[k].x = fma(r.x, sr, fma(-r.y, si, acc[k].x));
-          acc[k].y = fma(r.x, si, fma(r.y, sr, acc[k].y));
-        }
-      }
-      double met = ped + c0;
-      if (a.augmented) met -= a.noise_var * xs2;
-      if (a.full_labels) {
-        uint8_t* fl = a.full_labels + (gv * P + p) * n;
-        for (int k = 0; k < n; ++k) fl[k] = lab[k];
-        a.full_metrics[gv * P + p] = met;
-      }
-      if (ex_better(met, lab, bm, blab, n) || bp == 0x7fffffff) {
-        bm = met;
-        bp = p;
-        for (int k = 0; k < n; ++k) blab[k] = lab[k];
-      }
-    }
-    // ---- 4. block argmin on (metric, labels) ----
-    cm[tid] = bm;
-    cp[tid] = bp;
-    for (int k = 0; k < n; ++k) cl[tid * MPNL_MAX_N + k] = blab[k];
-    __syncthreads();
-    for (int s = EX_THREADS / 2; s > 0; s >>= 1) {
-      if (tid < s) {
-        const int o = tid + s;
-        const bool take = cp[o] != 0x7fffffff &&
-                          (cp[tid] == 0x7fffffff ||
-                           ex_better(cm[o], cl + o * MPNL_MAX_N, cm[tid], cl + tid * MPNL_MAX_N, n));
-        if (take) {
-          cm[tid] = cm[o];
-          cp[tid] = cp[o];
-          for (int k = 0; k < n; ++k) cl[tid * MPNL_MAX_N + k] = cl[o * MPNL_MAX_N + k];
-        }
-      }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      const uint8_t* wl = cl;
-      // Fix-up mode: when the fp64 winner equals the fp32 winner, keep the
-      // fp32 result untouched, so outputs never depend on which vectors a
-      // chunk-dependent guard happened to flag.
-      bool same = a.list != nullptr && a.hard != nullptr;
-      if (same)
-        for (int k = 0; k < n; ++k) same = same && a.hard[gv * n + k] == wl[k];
-      if (a.hard && !same)
-        for (int k = 0; k < n; ++k) a.hard[gv * n + k] = wl[k];
-      if (a.metric && !same) a.metric[gv] = (float)cm[0];
-      if (a.metric64) a.metric64[gv] = cm[0];
-      if (a.full_best) a.full_best[gv] = cp[0];
-    }
-    __syncthreads();
-  }
-}
+#define MPNL_DECL(LL, PP)                                                                 \
+  cudaError_t launch_exact_l##LL##_p##PP(int n, const ExactArgs& a, const TreeParams& tp, \
+                                         int grid, cudaStream_t st);
+MPNL_DECL(2, 0) MPNL_DECL(2, 1) MPNL_DECL(2, 2) MPNL_DECL(2, 3)
+MPNL_DECL(4, 0) MPNL_DECL(4, 1) MPNL_DECL(4, 2) MPNL_DECL(4, 3)
+MPNL_DECL(8, 0) MPNL_DECL(8, 1) MPNL_DECL(8, 2) MPNL_DECL(8, 3)
+#undef MPNL_DECL
 
 cudaError_t launch_exact(const ExactArgs& a, const TreeParams& tp, int grid, cudaStream_t st) {
-  const ExLayout lo(tp, a.n, a.L, a.exact_order);
-  const size_t smem = (size_t)lo.total;
-  cudaFuncSetAttribute(exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  exact_kernel<<<grid, EX_THREADS, smem, st>>>(a, tp);
-  return cudaGetLastError();
+  const int part = (a.n - 1) / 8;
+#define MPNL_PART(LL)                                                   \
+  switch (part) {                                                       \
+    case 0: return launch_exact_l##LL##_p0(a.n, a, tp, grid, st);      \
+    case 1: return launch_exact_l##LL##_p1(a.n, a, tp, grid, st);      \
+    case 2: return launch_exact_l##LL##_p2(a.n, a, tp, grid, st);      \
+    default: return launch_exact_l##LL##_p3(a.n, a, tp, grid, st);     \
+  }
+  if (a.L == 2) { MPNL_PART(2) }
+  if (a.L == 4) { MPNL_PART(4) }
+  MPNL_PART(8)
+#undef MPNL_PART
 }
 
 }  // namespace mpnl

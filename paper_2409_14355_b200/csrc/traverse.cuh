@@ -388,11 +388,21 @@ __device__ __forceinline__ void retrace_inline(const float* tab, int m, const fl
 #ifndef MPNL_PT_LARGE
 #define MPNL_PT_LARGE 1
 #endif
+#ifndef MPNL_MINB_SMALL
+#define MPNL_MINB_SMALL 0
+#endif
+#ifndef MPNL_MINB_MID
+#define MPNL_MINB_MID 0
+#endif
+#ifndef MPNL_MINB_LARGE
+#define MPNL_MINB_LARGE 0
+#endif
 template <int N>
 struct TravCfg {
   static constexpr int PT = N <= 8 ? MPNL_PT_SMALL : (N <= 16 ? MPNL_PT_MID : MPNL_PT_LARGE);
   static constexpr int MAXT = 128;                       // threads per CTA
-  static constexpr int MINB = PT * N <= 24 ? 4 : 3;      // CTAs per SM (no spills)
+  static constexpr int MB = N <= 8 ? MPNL_MINB_SMALL : (N <= 16 ? MPNL_MINB_MID : MPNL_MINB_LARGE);
+  static constexpr int MINB = MB ? MB : (PT * N <= 24 ? 4 : 3);   // CTAs per SM (no spills)
 };
 
 // mark vector gv for the fp64 kernel (the first marker appends it to the list)
@@ -411,6 +421,7 @@ __device__ __forceinline__ void send_to_fp64(const DetectArgs& a, int64_t gv, in
 
 __device__ __forceinline__ void log_event(const DetectArgs& a, int4 e) {
   const int idx = atomicAdd(a.counters + 1, 1);
+  if (a.stats) atomicAdd(a.stats, 1);
   if (idx < a.ev_cap) a.events[idx] = e;
   else send_to_fp64(a, (int64_t)(unsigned)e.z, 3);
 }
@@ -478,33 +489,40 @@ __device__ __forceinline__ void group_top3(Top3 t, int width, float& b1, unsigne
 }
 
 // ===========================================================================
-// K1b: per-vector preparation.  CTA = a channel's chunk of PREP_VC vectors:
-// the channel's fp64 Q^H (transposed), shift and layer table are staged once;
-// thread per (vector, row):  z'_k = fl32((Q^H y)_k - shift_k) with the rotation
-// in fp64, the per-layer guard threshold of the fp32 traversal; then thread per
-// vector: E_acc (L2 over layers) and the M > N metric offset (fixed-order sums).
+// K1b: per-vector preparation.  CTA = a channel's chunk of PREP_VC = 32
+// vectors, lane = vector, warp = block of 4 rows: the channel's fp64 Q^H
+// (transposed) is read as warp-uniform broadcasts, each lane's y_r feeds 4
+// rows.  z'_k = fl32((Q^H y)_k - shift_k) (fp64 rotation, one rounding), the
+// per-layer guard thresholds of the fp32 traversal, then per vector E_acc (L2
+// over layers) and the M > N metric offset (fixed-order sums).  Results are
+// staged in shared memory and written as contiguous rows.
 // ===========================================================================
 #define PREP_VC 32
+#define PREP_RB 4   // rows per warp
 
 struct PrepSmem {
-  int qt, sh, ly, y, e2, zn, total;   // bytes
+  int qt, sh, ly, y, z, th, e2, zn, total;   // bytes
   __host__ __device__ PrepSmem(int m, int n) {
+    const int npp = (n + 1) / 2, n4 = (n + 3) & ~3;
     int o = 0;
     qt = o; o += 16 * m * n;
     sh = o; o += 16 * n;
     ly = o; o += 16 * n;
-    y = o; o += 16 * PREP_VC * m;
+    y = o; o += 16 * PREP_VC * (m + 1);        // padded rows (bank spread)
+    z = o; o += 16 * PREP_VC * npp;            // staged z' rows (float2 per row)
+    th = o; o += 4 * PREP_VC * n4;             // staged thresholds
     e2 = o; o += 8 * PREP_VC * n;
     zn = o; o += 8 * PREP_VC * n;
     total = o;
   }
+  __host__ __device__ static int threads(int n) { return 32 * ((n + PREP_RB - 1) / PREP_RB); }
 };
 
 template <int N, int L>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
   (void)tparam;
-  constexpr int NPP = (N + 1) / 2;
+  constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
   extern __shared__ __align__(16) uint8_t psm[];
   const int m = a.m;
   const PrepSmem so(m, N);
@@ -512,6 +530,8 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
   double2* sh = reinterpret_cast<double2*>(psm + so.sh);
   float4* ly = reinterpret_cast<float4*>(psm + so.ly);
   double2* ys = reinterpret_cast<double2*>(psm + so.y);
+  float2* zst = reinterpret_cast<float2*>(psm + so.z);
+  float* tst = reinterpret_cast<float*>(psm + so.th);
   double* e2s = reinterpret_cast<double*>(psm + so.e2);
   double* zns = reinterpret_cast<double*>(psm + so.zn);
   const TableLayout tl(m, N);
@@ -519,171 +539,223 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
   const int v0 = (blockIdx.x % chunks) * PREP_VC;
   const int vce = (int)min((int64_t)PREP_VC, a.V - v0);
   const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const float* tab = a.tables + c * (int64_t)tl.total;
+  const int64_t g0 = c * a.V + v0;
   {
     const double2* q = reinterpret_cast<const double2*>(tab + tl.off_qh);
     for (int i = tid; i < m * N; i += nth) qt[i] = q[i];
     const double2* s2 = reinterpret_cast<const double2*>(tab + tl.off_shift);
     const float4* l4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
     for (int i = tid; i < N; i += nth) { sh[i] = s2[i]; ly[i] = l4[i]; }
-    const int64_t y0 = (c * a.V + v0) * (int64_t)m;
     for (int i = tid; i < vce * m; i += nth) {
+      const int v = i / m, r = i - v * m;
+      double2 yv;
       if (a.y_f64) {
-        ys[i] = reinterpret_cast<const double2*>(a.y)[y0 + i];
+        yv = reinterpret_cast<const double2*>(a.y)[g0 * m + i];
       } else {
-        const float2 v = reinterpret_cast<const float2*>(a.y)[y0 + i];
-        ys[i] = make_double2(v.x, v.y);
+        const float2 f = reinterpret_cast<const float2*>(a.y)[g0 * m + i];
+        yv = make_double2(f.x, f.y);
+      }
+      ys[v * (m + 1) + r] = yv;
+    }
+  }
+  __syncthreads();
+  const int v = lane;
+  const int k0 = warp * PREP_RB;
+  if (v < vce) {
+    const double2* yv = ys + v * (m + 1);
+    double zr[PREP_RB], zi[PREP_RB];
+#pragma unroll
+    for (int j = 0; j < PREP_RB; ++j) { zr[j] = 0.0; zi[j] = 0.0; }
+    double yn = 0.0;
+    for (int r = 0; r < m; ++r) {
+      const double2 y = yv[r];
+      yn = fma(y.x, y.x, fma(y.y, y.y, yn));
+#pragma unroll
+      for (int j = 0; j < PREP_RB; ++j) {
+        if (k0 + j < N) {
+          const double2 q = qt[r * N + k0 + j];   // warp-uniform broadcast
+          zr[j] = fma(q.x, y.x, zr[j]);
+          zr[j] = fma(-q.y, y.y, zr[j]);
+          zi[j] = fma(q.x, y.y, zi[j]);
+          zi[j] = fma(q.y, y.x, zi[j]);
+        }
+      }
+    }
+    const float ynf = (float)sqrt(yn) * 1.0001f;
+#pragma unroll
+    for (int j = 0; j < PREP_RB; ++j) {
+      const int k = k0 + j;
+      if (k < N) {
+        const float2 z = make_float2((float)(zr[j] - sh[k].x), (float)(zi[j] - sh[k].y));
+        zst[v * 2 * NPP + k] = z;   // (re, im) per row
+        const float4 lk = ly[k];
+        const float e = row_bound(ynf, z, lk, k, m, N, L, a.guard_scale, 0);
+        tst[v * N4 + k] = 0.5f - e / lk.y - MPNL_U * 2.f * L;
+        e2s[v * N + k] = (double)e * e;
+        zns[v * N + k] = zr[j] * zr[j] + zi[j] * zi[j];
       }
     }
   }
   __syncthreads();
-  // ||y|| per vector (fixed order), needed only for the tiny fp64 term of the bound
-  for (int it = tid; it < vce * N; it += nth) {
-    const int v = it / N, k = it - v * N;
-    const double2* yv = ys + v * m;
-    double zr = 0.0, zi = 0.0, yn = 0.0;
-    for (int r = 0; r < m; ++r) {
-      const double2 q = qt[r * N + k], y = yv[r];
-      zr = fma(q.x, y.x, zr);
-      zr = fma(-q.y, y.y, zr);
-      zi = fma(q.x, y.y, zi);
-      zi = fma(q.y, y.x, zi);
-      yn = fma(y.x, y.x, fma(y.y, y.y, yn));
-    }
-    const int64_t gv = c * a.V + v0 + v;
-    const float2 z = make_float2((float)(zr - sh[k].x), (float)(zi - sh[k].y));
-    reinterpret_cast<float2*>(a.zq + gv * NPP)[k] = z;   // (re, im) per row
-    const float e = row_bound((float)sqrt(yn) * 1.0001f, z, ly[k], k, m, N, L, a.guard_scale, 0);
-    a.thrg[gv * ((N + 3) & ~3) + k] = 0.5f - e / ly[k].y - MPNL_U * 2.f * L;
-    e2s[v * N + k] = (double)e * e;
-    zns[v * N + k] = zr * zr + zi * zi;
+  // contiguous write-out of the chunk's rows
+  {
+    const float4* zs4 = reinterpret_cast<const float4*>(zst);
+    float4* zo = a.zq + g0 * NPP;
+    for (int i = tid; i < vce * NPP; i += nth) zo[i] = zs4[i];
+    const float4* ts4 = reinterpret_cast<const float4*>(tst);
+    float4* to = reinterpret_cast<float4*>(a.thrg + g0 * N4);
+    for (int i = tid; i < vce * N4 / 4; i += nth) to[i] = ts4[i];
   }
-  __syncthreads();
-  for (int v = tid; v < vce; v += nth) {
-    const double2* yv = ys + v * m;
+  for (int vv = tid; vv < vce; vv += nth) {
+    const double2* yv = ys + vv * (m + 1);
     double yn = 0.0, e2 = 0.0, zn = 0.0;
     for (int r = 0; r < m; ++r) yn = fma(yv[r].x, yv[r].x, fma(yv[r].y, yv[r].y, yn));
-    for (int k = 0; k < N; ++k) { e2 += e2s[v * N + k]; zn += zns[v * N + k]; }
-    a.vaux[c * a.V + v0 + v] = make_float2((float)sqrt(e2) * 1.001f, (float)(yn - zn));
+    for (int k = 0; k < N; ++k) { e2 += e2s[vv * N + k]; zn += zns[vv * N + k]; }
+    a.vaux[g0 + vv] = make_float2((float)sqrt(e2) * 1.001f, (float)(yn - zn));
   }
 }
 
 // ===========================================================================
-// K2: partial-layer selection lists, one thread per (vector, parent)
+// K2: partial-layer selection lists
 // ===========================================================================
-template <int N, int L>
-__global__ void __launch_bounds__(128)
-select_kernel(const DetectArgs a, const TreeParams tparam, int pos) {
-  constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
-  __shared__ TreeParams tp;
-  __shared__ float scratch[20 * 128];
-  {
-    const int* s = reinterpret_cast<const int*>(&tparam);
-    int* d = reinterpret_cast<int*>(&tp);
-    for (int i = threadIdx.x; i < (int)(sizeof(TreeParams) / 4); i += blockDim.x) d[i] = s[i];
+// K2 (templated on the expansion count E of the partial layer): one thread per
+// (vector, parent), block = (parents, vectors).  The E nearest points of the
+// centre are the E smallest sums dx_i + dy_j of the two per-axis
+// Schnorr-Euchner distance orders (only the SET matters for hard output): a
+// register-resident k-smallest-sums merge, E + 1 picks (the (E+1)-th sum is
+// the guard's cut partner).
+template <int K, typename T>
+__device__ __forceinline__ T dyn_at(const T (&v)[K], int i) {
+  T r = v[0];
+#pragma unroll
+  for (int k = 1; k < K; ++k) r = (i == k) ? v[k] : r;
+  return r;
+}
+
+// per-axis levels sorted by distance to x (level-index units): lev[r], d[r]
+template <int L>
+__device__ __forceinline__ void se_order(float x, int (&lev)[L], float (&d)[L]) {
+  const int n0 = (int)rintf(fminf(fmaxf(x, 0.f), (float)(L - 1)));
+  int lo = n0 - 1, hi = n0 + 1;
+  lev[0] = n0;
+  d[0] = (x - n0) * (x - n0);
+#pragma unroll
+  for (int r = 1; r < L; ++r) {
+    const bool up = (hi < L) && (lo < 0 || (hi - x) < (x - lo));
+    const int l = up ? hi : lo;
+    hi += up ? 1 : 0;
+    lo -= up ? 0 : 1;
+    lev[r] = l;
+    d[r] = (x - l) * (x - l);
   }
-  __syncthreads();
+}
+
+template <int N, int L, int EMAX>
+__global__ void __launch_bounds__(128)
+select_kernel(const DetectArgs a, const TreeParams tp, int pos) {
+  const int E = tp.e[pos];   // <= EMAX
+  constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
+  constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
   const float INF = __int_as_float(0x7f800000);
-  const int m = a.m;
-  const TableLayout tl(m, N);
-  const int e = tp.e[pos];
   const int npar = tp.n_paths / tp.stride[pos + 1];
+  const int par = blockIdx.y * blockDim.x + threadIdx.x;
   const int64_t B = a.n_ch * a.V;
-  const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (item >= B * npar) return;
-  const int64_t gv = item / npar;
-  const int par = (int)(item - gv * npar);
-  const int64_t c = gv / a.V;
-  const float* tab = a.tables + c * (int64_t)tl.total;
-  const TabPtrs T = tab_ptrs(tab, m, N);
+  const int64_t gv = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (par >= npar || gv >= B) return;
+  const int c = (int)(gv / a.V);
+  const float* tab = a.tables + (int64_t)c * TableLayout(a.m, N).total;
+  const TabPtrs T = tab_ptrs(tab, a.m, N);
   const int p0 = par * tp.stride[pos + 1];
   uint8_t* vlist = a.lists + gv * tp.list_bytes;
-  const float* zrow = reinterpret_cast<const float*>(a.zq + gv * ((N + 1) / 2));
-  // prefix symbols (expanded layers above pos)
-  float sr[XM], si[XM];
+  // acc of row pos after the expanded layers above it (the traversal's fma order)
+  const float2 z = reinterpret_cast<const float2*>(a.zq + gv * NPP)[pos];
+  float xr = z.x, xi = z.y;
 #pragma unroll
   for (int q = 0; q < XM; ++q) {
     const int j = N - 1 - q;
-    sr[q] = 0.f; si[q] = 0.f;
     if (j > pos) {
       int ir, ii;
       expanded_symbol<L>(tp, j, p0, vlist, ir, ii);
-      sr[q] = (float)ir; si[q] = (float)ii;
+      const float2 r2 = rcol_at(T.rcol, NPP, pos, j);
+      acc_step(xr, xi, r2.x, r2.y, (float)ir, (float)ii);
     }
   }
-  // acc at pos in traversal order (z' from the prep kernel)
-  float xr = 0.f, xi = 0.f;
-#pragma unroll
-  for (int q = 0; q < XM; ++q) {
-    const int j = N - 1 - q;
-    if (j != pos) continue;
-    float ar_ = zrow[2 * j], ai_ = zrow[2 * j + 1];
-#pragma unroll
-    for (int q2 = 0; q2 < q; ++q2) {
-      const int l = N - 1 - q2;
-      const float2 r2 = rcol_at(T.rcol, (N + 1) / 2, j, l);
-      acc_step(ar_, ai_, r2.x, r2.y, sr[q2], si[q2]);
-    }
-    xr = ar_;
-    xi = ai_;
-  }
-  const float4 lyp = T.lay4[pos];
-  // index-domain centre error bound (prep kernel) for the cut guard
-  const float E = 0.5f - a.thrg[gv * ((N + 3) & ~3) + pos];
-  // centre in level-index units (unclamped)
-  const float cx = __fmul_rn(xr, lyp.x);
-  const float cy = __fmul_rn(xi, lyp.x);
-  // per-axis closest-first level orders in a transposed per-thread scratch
-  const int nth = blockDim.x;
-  float* scr = scratch + threadIdx.x;
-  uint8_t* sox = reinterpret_cast<uint8_t*>(scr + 16 * nth);
-  uint8_t* soy = reinterpret_cast<uint8_t*>(scr + 18 * nth);
-#pragma unroll
-  for (int ax = 0; ax < 2; ++ax) {
-    const float x = ax ? cy : cx;
-    const int n0 = (int)rintf(fminf(fmaxf(x, 0.f), (float)(L - 1)));
-    int lo = n0 - 1, hi = n0 + 1;
-    float* dd = scr + (ax ? 8 : 0) * nth;
-    uint8_t* oo = ax ? soy : sox;
-    oo[0] = (uint8_t)n0;
-    dd[0] = (x - n0) * (x - n0);
-#pragma unroll
-    for (int r = 1; r < L; ++r) {
-      const bool up = (hi < L) && (lo < 0 || (hi - x) < (x - lo));
-      const int lev = up ? hi : lo;
-      hi += up ? 1 : 0;
-      lo -= up ? 0 : 1;
-      oo[(r & 3) + (r >> 2) * 4 * nth] = (uint8_t)lev;
-      dd[r * nth] = (x - lev) * (x - lev);
-    }
-  }
-  auto ldx = [&](int i) { return scr[i * nth]; };
-  auto ldy = [&](int j) { return scr[(8 + j) * nth]; };
-  auto lox = [&](int i) { return (int)sox[(i & 3) + (i >> 2) * 4 * nth]; };
-  auto loy = [&](int j) { return (int)soy[(j & 3) + (j >> 2) * 4 * nth]; };
-  // k-smallest sums dx[i] + dy[w_i] (rows sorted): e members + the (e+1)-th
+  const float kx = T.lay4[pos].x;
+  const float Eb = 0.5f - a.thrg[gv * N4 + pos];   // index-domain centre error bound
+  int ox[L], oy[L];
+  float dx[L], dy[L];
+  se_order<L>(__fmul_rn(xr, kx), ox, dx);
+  se_order<L>(__fmul_rn(xi, kx), oy, dy);
   int w[L];
   float nk[L];
-  const float dy0 = ldy(0);
 #pragma unroll
-  for (int i = 0; i < L; ++i) { w[i] = 0; nk[i] = ldx(i) + dy0; }
+  for (int i = 0; i < L; ++i) { w[i] = 0; nk[i] = dx[i] + dy[0]; }
+  constexpr int NW = (EMAX + 3) / 4;
+  unsigned words[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) words[i] = 0u;
   float kprev = 0.f, knext = 0.f;
-  uint8_t* out = vlist + tp.list_off[pos] + par * e;
-  for (int pick = 0; pick <= e; ++pick) {
-    int sel = 0, col = w[0];
+  // L = 8: the per-axis orders live in per-thread (transposed) shared memory,
+  // so the merge's data-dependent lookups are single LDS instead of select chains
+  constexpr bool SMEM = L == 8;
+  __shared__ float sdx[SMEM ? L : 1][128], sdy[SMEM ? L : 1][128];
+  __shared__ uint8_t sox[SMEM ? L : 1][128], soy[SMEM ? L : 1][128], sw[SMEM ? L : 1][128];
+  const int th = threadIdx.y * blockDim.x + threadIdx.x;
+  if (SMEM) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      sdx[i][th] = dx[i]; sdy[i][th] = dy[i];
+      sox[i][th] = (uint8_t)ox[i]; soy[i][th] = (uint8_t)oy[i]; sw[i][th] = 0;
+    }
+  }
+#pragma unroll
+  for (int pick = 0; pick <= EMAX; ++pick) {
+    if (pick > E) break;
+    int sel = 0;
     float best = nk[0];
 #pragma unroll
-    for (int i = 1; i < L; ++i)
-      if (nk[i] < best) { best = nk[i]; sel = i; col = w[i]; }
-    if (pick < e) { out[pick] = (uint8_t)((lox(sel) << 3) | loy(col)); kprev = best; }
-    else knext = best;
-    const float nxt = (col + 1 < L) ? ldx(sel) + ldy(col + 1) : INF;
+    for (int i = 1; i < L; ++i) {
+      const bool lt = nk[i] < best;
+      best = lt ? nk[i] : best;
+      sel = lt ? i : sel;
+    }
+    if (pick < E) {
+      int col;
+      unsigned b;
+      float nxt;
+      if (SMEM) {
+        col = sw[sel][th];
+        b = ((unsigned)sox[sel][th] << 3) | (unsigned)soy[col][th];
+        nxt = (col + 1 < L) ? sdx[sel][th] + sdy[col + 1][th] : INF;
+        sw[sel][th] = (uint8_t)(col + 1);
+      } else {
+        col = dyn_at(w, sel);
+        b = (unsigned)((dyn_at(ox, sel) << 3) | dyn_at(oy, col));
+        nxt = (col + 1 < L) ? dyn_at(dx, sel) + dyn_at(dy, col + 1) : INF;
+      }
+      words[pick >> 2] |= b << (8 * (pick & 3));
+      kprev = best;
 #pragma unroll
-    for (int i = 0; i < L; ++i)
-      if (i == sel) { w[i] = col + 1; nk[i] = nxt; }
+      for (int i = 0; i < L; ++i)
+        if (i == sel) { if (!SMEM) w[i] = col + 1; nk[i] = nxt; }
+    } else {
+      knext = best;
+    }
+  }
+  uint8_t* out = vlist + tp.list_off[pos] + par * E;
+  if ((E & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+      if (4 * i < E) reinterpret_cast<unsigned*>(out)[i] = words[i];
+  } else {
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k)
+      if (k < E) out[k] = (uint8_t)(words[k >> 2] >> (8 * (k & 3)));
   }
   // cut guard: distance keys are within 2 sqrt2 E (sqrt k) + 2E^2 (+ rounding)
-  const float bound = 2.8284272f * E * (sqrtf(kprev) + sqrtf(knext)) + 4.f * E * E +
+  const float bound = 2.8284272f * Eb * (sqrtf(kprev) + sqrtf(knext)) + 4.f * Eb * Eb +
                       8.f * MPNL_U * (knext + 1.f);
   if (knext - kprev <= bound) log_event(a, make_int4(p0, pos, (int)gv, EV_CUT));
 }
@@ -842,8 +914,21 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       const int vce = min(nvi, V - jv);
 
       Top3 run = {INF, INF, INF, 0xffffffffu, 0xffffffffu};
-      float wbest = INF;   // warp-wide best so far of this vector (multi-batch)
-      for (int b = 0; b < bpv; ++b) {
+      float wbest = INF;   // warp-wide best so far of this vector
+      // multi-batch: start with the batch holding the top layer's nearest point
+      // (the SIC family), so the event filter has a good bound from the start;
+      // the result does not depend on the batch order (total order on paths)
+      int b0 = 0;
+      if (!VPI && bpv > 1 && tp.e[N - 1] == L * L) {
+        const float4 zt = zs[(N - 1) >> 1];
+        const float ur = ((N - 1) & 1) ? zt.z : zt.x, ui = ((N - 1) & 1) ? zt.w : zt.y;
+        float t0;
+        const float kxt = T.lay4[N - 1].x;
+        const int d0 = (int)slice_axis<L>(ur, kxt, t0) * L + (int)slice_axis<L>(ui, kxt, t0);
+        b0 = (d0 * tp.stride[N - 1]) / S;
+      }
+      for (int bi = 0; bi < bpv; ++bi) {
+        const int b = (VPI || bpv == 1) ? 0 : (b0 + bi < bpv ? b0 + bi : b0 + bi - bpv);
         int vl[PT], pp[PT];
         int64_t gvl[PT];
         bool ok[PT];
@@ -867,6 +952,12 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         traverse_paths<N, L, PT, true, false, !VPI>(T, zs, thr, lch, tp, lbytes, vl, gvl, pp, ped,
                                                     evm, evp, nullptr, nullptr, -1,
                                                     use_xs ? xs : nullptr);
+        if (!VPI) {   // the bound includes this batch's own best
+          float bm = INF;
+#pragma unroll
+          for (int t = 0; t < PT; ++t) bm = ok[t] ? fminf(bm, ped[t]) : bm;
+          wbest = fminf(wbest, __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(bm))));
+        }
         // log paths with a marked decision whose prefix may still be competitive
 #pragma unroll
         for (int t = 0; t < PT; ++t) {
@@ -884,8 +975,6 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
 #pragma unroll
           for (int t = 0; t < PT; ++t)
             if (ok[t]) top3_insert(run, ped[t], (unsigned)pp[t]);
-          if (bpv > 1)
-            wbest = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
         } else if (P >= 32) {
           const int g = P >> 5;   // t-slots per vector
 #pragma unroll
@@ -936,7 +1025,10 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   // ---- flush the CTA's event buffer to the global log ----
   __syncthreads();
   const int n_ev = min(evn[0], TRAV_EV_CAP);
-  if (tid == 0) evn[1] = n_ev ? atomicAdd(a.counters + 1, n_ev) : 0;
+  if (tid == 0) {
+    evn[1] = n_ev ? atomicAdd(a.counters + 1, n_ev) : 0;
+    if (a.stats && n_ev) atomicAdd(a.stats, n_ev);
+  }
   __syncthreads();
   const int base = evn[1];
   for (int i = tid; i < n_ev; i += nth) {

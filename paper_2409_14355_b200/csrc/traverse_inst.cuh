@@ -5,6 +5,7 @@
 #pragma once
 #include <algorithm>
 
+#include "exact.cuh"
 #include "traverse.cuh"
 
 namespace mpnl {
@@ -15,7 +16,22 @@ template <int NN, int L>
 cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp, unsigned grid,
                             int threads, size_t smem, int extra, cudaStream_t st) {
   if (kind == 0) {
-    select_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
+    // block = (parents, vectors); the smallest unrolled pick count >= e
+    const int pos = extra, e = tp.e[pos];
+    const int npar = tp.n_paths / tp.stride[pos + 1];
+    const int px = std::min(npar, 128), vy = std::max(1, 128 / px);
+    const int64_t B = a.n_ch * a.V;
+    const dim3 blk(px, vy), grd((unsigned)((B + vy - 1) / vy), (unsigned)((npar + px - 1) / px));
+    if constexpr (L == 2) {
+      select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos);
+    } else if constexpr (L == 4) {
+      if (e <= 4) select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos);
+      else select_kernel<NN, L, 16><<<grd, blk, 0, st>>>(a, tp, pos);
+    } else {
+      if (e <= 4) select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos);
+      else if (e <= 16) select_kernel<NN, L, 16><<<grd, blk, 0, st>>>(a, tp, pos);
+      else select_kernel<NN, L, 64><<<grd, blk, 0, st>>>(a, tp, pos);
+    }
   } else if (kind == 1) {
     // persistent: grid = resident capacity (capped by the item count `extra`)
     auto k = a.vpi > 1 ? traverse_kernel<NN, L, true> : traverse_kernel<NN, L, false>;
@@ -46,6 +62,18 @@ cudaError_t launch_fast_part(int n, int kind, const DetectArgs& a, const TreePar
   switch (n - N0) {
 #define MPNL_C(I) \
     case I: return launch_fast_one<N0 + I, L>(kind, a, tp, grid, threads, smem, extra, st);
+    MPNL_C(0) MPNL_C(1) MPNL_C(2) MPNL_C(3) MPNL_C(4) MPNL_C(5) MPNL_C(6) MPNL_C(7)
+#undef MPNL_C
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int L, int N0>
+cudaError_t launch_exact_part(int n, const ExactArgs& a, const TreeParams& tp, int grid,
+                              cudaStream_t st) {
+  switch (n - N0) {
+#define MPNL_C(I) \
+    case I: return launch_exact_t<N0 + I, L>(a, tp, grid, st);
     MPNL_C(0) MPNL_C(1) MPNL_C(2) MPNL_C(3) MPNL_C(4) MPNL_C(5) MPNL_C(6) MPNL_C(7)
 #undef MPNL_C
     default: return cudaErrorInvalidValue;

@@ -1,4 +1,4 @@
-// Generated: fast-path kernels for 4-QAM, N = 17..24.
+// Generated: fast-path and fp64 kernels for 4-QAM, N = 17..24.
 #include "traverse_inst.cuh"
 
 namespace mpnl {
@@ -6,5 +6,9 @@ cudaError_t launch_fast_l2_p2(int n, int kind, const DetectArgs& a, const TreePa
                                     unsigned grid, int threads, size_t smem, int extra,
                                     cudaStream_t st) {
   return launch_fast_part<2, 17>(n, kind, a, tp, grid, threads, smem, extra, st);
+}
+cudaError_t launch_exact_l2_p2(int n, const ExactArgs& a, const TreeParams& tp, int grid,
+                                     cudaStream_t st) {
+  return launch_exact_part<2, 17>(n, a, tp, grid, st);
 }
 }  // namespace mpnl

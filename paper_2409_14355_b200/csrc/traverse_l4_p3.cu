@@ -1,4 +1,4 @@
-// Generated: fast-path kernels for 16-QAM, N = 25..32.
+// Generated: fast-path and fp64 kernels for 16-QAM, N = 25..32.
 #include "traverse_inst.cuh"
 
 namespace mpnl {
@@ -6,5 +6,9 @@ cudaError_t launch_fast_l4_p3(int n, int kind, const DetectArgs& a, const TreePa
                                     unsigned grid, int threads, size_t smem, int extra,
                                     cudaStream_t st) {
   return launch_fast_part<4, 25>(n, kind, a, tp, grid, threads, smem, extra, st);
+}
+cudaError_t launch_exact_l4_p3(int n, const ExactArgs& a, const TreeParams& tp, int grid,
+                                     cudaStream_t st) {
+  return launch_exact_part<4, 25>(n, a, tp, grid, st);
 }
 }  // namespace mpnl

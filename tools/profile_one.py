@@ -25,5 +25,5 @@ for _ in range(reps):
 torch.cuda.synchronize()
 nv_ = y.shape[0] * y.shape[1]
 print(name, "vectors", nv_, "flag rate", float(flags.float().mean()),
-      "per vector: checked %.3f ties %.4f flagged %.5f [3way %.5f f64tie %.5f mismatch %.5f overflow %.5f]" % tuple(
-          x / reps / nv_ for x in stats.tolist()[1:]))
+      "per vector: events %.4f checked %.4f ties %.4f flagged %.5f [3way %.5f f64tie %.5f mismatch %.5f overflow %.5f]" % tuple(
+          x / reps / nv_ for x in stats.tolist()))
