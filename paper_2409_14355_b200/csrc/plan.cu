@@ -10,10 +10,12 @@
 //   * r_kk recomputed from the pivot column, floored at 1e-300 (348-350);
 //   * Q^H = top M rows of Q, conjugate-transposed (383).
 //
-// B200 mapping: one warp per channel, lane j owns *physical* column j of A in
-// shared memory (A[m][j], lane-contiguous, conflict-free).  Column swaps are
-// pure bookkeeping (each lane tracks the logical position of its column), so
-// no data moves.  Row reductions (r_kk) are warp reductions over rows.
+// B200 mapping: one 4-warp CTA per channel.  Lane j owns *physical* column j
+// of A in shared memory (A[m][j], padded rows); the column bookkeeping (norms,
+// logical positions) is replicated identically in every warp, so column swaps
+// are pure bookkeeping and no data moves.  Each warp owns a quarter of the
+// rows for the projections and updates (partials summed in a fixed order);
+// r_kk is a block reduction over rows.
 // Everything is fp64; the fast path's fp32 tables are derived at the end.
 #include "common.cuh"
 
@@ -37,43 +39,57 @@ __device__ inline double warp_sum_d(double v) {
   return v;
 }
 
+#define PLAN_THREADS 128
+#define PLAN_WARPS (PLAN_THREADS / 32)
+
 template <typename TIn>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(PLAN_THREADS)
 plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
                double noise_var, int augmented, int32_t* __restrict__ perm_out,
                double2* __restrict__ r_out, double2* __restrict__ qh_out,
                float* __restrict__ tables) {
   extern __shared__ double2 smem[];
   const int ma = augmented ? m + n : m;
-  double2* A = smem;              // [ma][n] physical columns
-  double2* Rp = smem + ma * n;    // [n][n] rows of R by physical column
+  const int ns = n + 1;           // padded row stride: row-parallel column access spreads banks
+  double2* A = smem;              // [ma][ns] physical columns
+  double2* Rp = smem + ma * ns;   // [n][n] rows of R by physical column
+  double2* red = Rp + n * n;      // [PLAN_WARPS][32] partial dot products
+  double* rkp = reinterpret_cast<double*>(red + PLAN_WARPS * 32);   // [PLAN_WARPS] partial norms
   const int64_t c = blockIdx.x;
   if (c >= n_ch) return;
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
-  // ---- load A (row-parallel, coalesced over the (m, n) row-major input) ----
+  // ---- load A (coalesced over the (m, n) row-major input) ----
   const TIn* hc = h + c * (int64_t)m * n;
-  for (int idx = lane; idx < m * n; idx += 32) A[idx] = load_c<TIn>(hc, idx);
+  for (int idx = tid; idx < m * n; idx += PLAN_THREADS) {
+    const int r = idx / n, j = idx - r * n;
+    A[r * ns + j] = load_c<TIn>(hc, idx);
+  }
   if (augmented) {
     const double s = sqrt(noise_var);
-    for (int idx = lane; idx < n * n; idx += 32) {
+    for (int idx = tid; idx < n * n; idx += PLAN_THREADS) {
       int i = idx / n, j = idx % n;
-      A[(m + i) * n + j] = make_double2(i == j ? s : 0.0, 0.0);
+      A[(m + i) * ns + j] = make_double2(i == j ? s : 0.0, 0.0);
     }
   }
-  for (int idx = lane; idx < n * n; idx += 32) Rp[idx] = make_double2(0.0, 0.0);
-  __syncwarp();
+  for (int idx = tid; idx < n * n; idx += PLAN_THREADS) Rp[idx] = make_double2(0.0, 0.0);
+  __syncthreads();
 
+  // Column bookkeeping, replicated identically in every warp: lane j owns
+  // physical column j (norm, logical position, chosen).
   const bool own = lane < n;
   double norm = 0.0;
   if (own)
     for (int r = 0; r < ma; ++r) {
-      double2 a = A[r * n + lane];
+      double2 a = A[r * ns + lane];
       norm = fma(a.x, a.x, fma(a.y, a.y, norm));
     }
   int logpos = lane;     // logical position of my physical column
   bool chosen = !own;
   int my_final = -1;     // final logical position (== step at which chosen)
+  // rows of this warp for the column updates
+  const int rb = (ma + PLAN_WARPS - 1) / PLAN_WARPS;
+  const int r0 = w * rb, r1 = min(ma, r0 + rb);
 
   for (int k = 0; k < n; ++k) {
     // pivot: max downdated norm, ties -> smallest logical position (first max)
@@ -93,76 +109,96 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     if (!chosen && logpos == k) logpos = cp_pos;
     if (lane == cp) { logpos = k; chosen = true; my_final = k; }
 
-    // r_kk from the pivot column (row-parallel reduction)
+    // r_kk from the pivot column (thread per row, fixed-order block reduction)
     double part = 0.0;
-    for (int r = lane; r < ma; r += 32) {
-      double2 a = A[r * n + cp];
-      part = fma(a.x, a.x, fma(a.y, a.y, part));
+    if (tid < ma) {
+      const double2 a = A[tid * ns + cp];
+      part = fma(a.x, a.x, a.y * a.y);
     }
-    double rkk = fmax(sqrt(warp_sum_d(part)), 1e-300);
-    __syncwarp();
-    for (int r = lane; r < ma; r += 32) {
-      double2 a = A[r * n + cp];
-      A[r * n + cp] = make_double2(a.x / rkk, a.y / rkk);
+    part = warp_sum_d(part);
+    if (lane == 0) rkp[w] = part;
+    __syncthreads();
+    double ss = 0.0;
+#pragma unroll
+    for (int i = 0; i < PLAN_WARPS; ++i) ss += rkp[i];
+    const double rkk = fmax(sqrt(ss), 1e-300);
+    if (tid < ma) {
+      const double2 a = A[tid * ns + cp];
+      A[tid * ns + cp] = make_double2(a.x / rkk, a.y / rkk);
     }
-    if (lane == 0) Rp[k * n + cp] = make_double2(rkk, 0.0);
-    __syncwarp();
+    if (tid == 0) Rp[k * n + cp] = make_double2(rkk, 0.0);
+    __syncthreads();
+    // proj_j = q^H a_j over this warp's rows -> partials -> fixed-order sum
+    double pr = 0.0, pi = 0.0;
     if (!chosen) {
-      // proj = q^H a_j ; a_j -= q proj ; norm -= |proj|^2
-      double pr = 0.0, pi = 0.0;
-      for (int r = 0; r < ma; ++r) {
-        double2 q = A[r * n + cp];
-        double2 a = A[r * n + lane];
+      double pr2 = 0.0, pi2 = 0.0;
+      int r = r0;
+      for (; r + 2 <= r1; r += 2) {
+        const double2 q = A[r * ns + cp], a = A[r * ns + lane];
+        const double2 q2 = A[(r + 1) * ns + cp], a2 = A[(r + 1) * ns + lane];
         pr = fma(q.x, a.x, fma(q.y, a.y, pr));      // conj(q) * a
         pi = fma(q.x, a.y, fma(-q.y, a.x, pi));
+        pr2 = fma(q2.x, a2.x, fma(q2.y, a2.y, pr2));
+        pi2 = fma(q2.x, a2.y, fma(-q2.y, a2.x, pi2));
       }
-      Rp[k * n + lane] = make_double2(pr, pi);
-      for (int r = 0; r < ma; ++r) {
-        double2 q = A[r * n + cp];
-        double2 a = A[r * n + lane];
+      if (r < r1) {
+        const double2 q = A[r * ns + cp], a = A[r * ns + lane];
+        pr = fma(q.x, a.x, fma(q.y, a.y, pr));
+        pi = fma(q.x, a.y, fma(-q.y, a.x, pi));
+      }
+      red[w * 32 + lane] = make_double2(pr + pr2, pi + pi2);
+    }
+    __syncthreads();
+    if (!chosen) {
+      pr = 0.0;
+      pi = 0.0;
+#pragma unroll
+      for (int i = 0; i < PLAN_WARPS; ++i) { pr += red[i * 32 + lane].x; pi += red[i * 32 + lane].y; }
+      if (w == 0) Rp[k * n + lane] = make_double2(pr, pi);
+      for (int rr = r0; rr < r1; ++rr) {
+        const double2 q = A[rr * ns + cp];
+        double2 a = A[rr * ns + lane];
         a.x -= q.x * pr - q.y * pi;
         a.y -= q.x * pi + q.y * pr;
-        A[r * n + lane] = a;
+        A[rr * ns + lane] = a;
       }
       norm = fmax(norm - (pr * pr + pi * pi), 0.0);
     }
-    __syncwarp();
+    __syncthreads();
   }
 
   // ---- outputs in logical order ----
-  // phys_of[logical] via shuffles: lane j (physical) knows my_final.
   __shared__ int phys_of[MPNL_MAX_N];
-  if (own) phys_of[my_final] = lane;
-  __syncwarp();
+  if (w == 0 && own) phys_of[my_final] = lane;
+  __syncthreads();
   int32_t* pc = perm_out + c * n;
   double2* rc = r_out + c * (int64_t)n * n;
   double2* qc = qh_out + c * (int64_t)n * m;
-  for (int idx = lane; idx < n; idx += 32) pc[idx] = phys_of[idx];
-  for (int idx = lane; idx < n * n; idx += 32) {
+  for (int idx = tid; idx < n; idx += PLAN_THREADS) pc[idx] = phys_of[idx];
+  for (int idx = tid; idx < n * n; idx += PLAN_THREADS) {
     int i = idx / n, j = idx % n;
     rc[idx] = (j >= i) ? Rp[i * n + phys_of[j]] : make_double2(0.0, 0.0);
   }
-  for (int idx = lane; idx < n * m; idx += 32) {
+  for (int idx = tid; idx < n * m; idx += PLAN_THREADS) {
     int k = idx / m, r = idx % m;
-    double2 q = A[r * n + phys_of[k]];
+    double2 q = A[r * ns + phys_of[k]];
     qc[idx] = make_double2(q.x, -q.y);
   }
 
   // ---- fp32 traversal tables (see TableLayout) ----
   if (tables == nullptr) return;
-  __syncwarp();
   TableLayout tl(m, n);
   float* tc = tables + c * (int64_t)tl.total;
   const double nrm = qam_norm_d(L);
   const double sc = 2.0 / nrm;
   const double lv = (double)(L - 1) / nrm;
   double2* qt = reinterpret_cast<double2*>(tc + tl.off_qh);
-  for (int idx = lane; idx < n * m; idx += 32) {
+  for (int idx = tid; idx < n * m; idx += PLAN_THREADS) {
     int r = idx / n, k = idx % n;       // transposed: qhT[r][k] = conj(q_k[r])
-    double2 q = A[r * n + phys_of[k]];
+    double2 q = A[r * ns + phys_of[k]];
     qt[idx] = make_double2(q.x, -q.y);
   }
-  for (int idx = lane; idx < n * 2 * tl.npp; idx += 32) {
+  for (int idx = tid; idx < n * 2 * tl.npp; idx += PLAN_THREADS) {
     const int pos = idx / (2 * tl.npp), k = idx % (2 * tl.npp);   // column pos, row k
     float2 v = make_float2(0.f, 0.f);
     if (k < pos) {
@@ -173,7 +209,7 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     blk[0] = v.x;   // {rr_2q, ri_2q, rr_2q+1, ri_2q+1}
     blk[1] = v.y;
   }
-  for (int k = lane; k < n; k += 32) {
+  for (int k = tid; k < n; k += PLAN_THREADS) {
     double sr = 0.0, si = 0.0, sabs = 0.0;
     for (int j = k; j < n; ++j) {
       double2 r = Rp[k * n + phys_of[j]];
@@ -204,17 +240,18 @@ cudaError_t launch_plan(const void* h, int h_is_f64, int64_t n_ch, int m, int n,
                         double noise_var, int augmented, int32_t* perm, double2* r64,
                         double2* qh64, float* tables, cudaStream_t st) {
   const int ma = augmented ? m + n : m;
-  size_t smem = (size_t)(ma * n + n * n) * sizeof(double2);
+  size_t smem = (size_t)(ma * (n + 1) + n * n + PLAN_WARPS * 32) * sizeof(double2) +
+                PLAN_WARPS * sizeof(double);
   if (n_ch == 0) return cudaSuccess;
   if (h_is_f64) {
     cudaFuncSetAttribute(plan_qr_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    plan_qr_kernel<double2><<<(unsigned)n_ch, 32, smem, st>>>(
+    plan_qr_kernel<double2><<<(unsigned)n_ch, PLAN_THREADS, smem, st>>>(
         (const double2*)h, n_ch, m, n, L, noise_var, augmented, perm, r64, qh64, tables);
   } else {
     cudaFuncSetAttribute(plan_qr_kernel<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    plan_qr_kernel<float2><<<(unsigned)n_ch, 32, smem, st>>>(
+    plan_qr_kernel<float2><<<(unsigned)n_ch, PLAN_THREADS, smem, st>>>(
         (const float2*)h, n_ch, m, n, L, noise_var, augmented, perm, r64, qh64, tables);
   }
   return cudaGetLastError();

@@ -509,10 +509,10 @@ struct PrepSmem {
     sh = o; o += 16 * n;
     ly = o; o += 16 * n;
     y = o; o += 16 * PREP_VC * (m + 1);        // padded rows (bank spread)
-    z = o; o += 16 * PREP_VC * npp;            // staged z' rows (float2 per row)
-    th = o; o += 4 * PREP_VC * n4;             // staged thresholds
-    e2 = o; o += 8 * PREP_VC * n;
-    zn = o; o += 8 * PREP_VC * n;
+    z = o; o += 8 * PREP_VC * (2 * npp + 1);   // staged z' rows (float2, padded stride)
+    th = o; o += 4 * PREP_VC * (n4 + 1);       // staged thresholds (padded stride)
+    e2 = o; o += 8 * PREP_VC * 9;              // per (row block, vector) partial sums; [8]: ||y||^2
+    zn = o; o += 8 * PREP_VC * 8;
     total = o;
   }
   __host__ __device__ static int threads(int n) { return 32 * ((n + PREP_RB - 1) / PREP_RB); }
@@ -584,35 +584,44 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
       }
     }
     const float ynf = (float)sqrt(yn) * 1.0001f;
+    double e2p = 0.0, znp = 0.0;
 #pragma unroll
     for (int j = 0; j < PREP_RB; ++j) {
       const int k = k0 + j;
       if (k < N) {
         const float2 z = make_float2((float)(zr[j] - sh[k].x), (float)(zi[j] - sh[k].y));
-        zst[v * 2 * NPP + k] = z;   // (re, im) per row
+        zst[v * (2 * NPP + 1) + k] = z;   // (re, im) per row
         const float4 lk = ly[k];
         const float e = row_bound(ynf, z, lk, k, m, N, L, a.guard_scale, 0);
-        tst[v * N4 + k] = 0.5f - e / lk.y - MPNL_U * 2.f * L;
-        e2s[v * N + k] = (double)e * e;
-        zns[v * N + k] = zr[j] * zr[j] + zi[j] * zi[j];
+        tst[v * (N4 + 1) + k] = 0.5f - e / lk.y - MPNL_U * 2.f * L;
+        e2p += (double)e * e;
+        znp += zr[j] * zr[j] + zi[j] * zi[j];
       }
     }
+    e2s[warp * PREP_VC + v] = e2p;
+    zns[warp * PREP_VC + v] = znp;
+    if (warp == 0) e2s[8 * PREP_VC + v] = yn;
   }
   __syncthreads();
-  // contiguous write-out of the chunk's rows
+  // contiguous write-out of the chunk's rows (un-padding the staged strides)
   {
-    const float4* zs4 = reinterpret_cast<const float4*>(zst);
-    float4* zo = a.zq + g0 * NPP;
-    for (int i = tid; i < vce * NPP; i += nth) zo[i] = zs4[i];
-    const float4* ts4 = reinterpret_cast<const float4*>(tst);
-    float4* to = reinterpret_cast<float4*>(a.thrg + g0 * N4);
-    for (int i = tid; i < vce * N4 / 4; i += nth) to[i] = ts4[i];
+    float2* zo = reinterpret_cast<float2*>(a.zq + g0 * NPP);
+    for (int i = tid; i < vce * 2 * NPP; i += nth) {
+      const int vv = i / (2 * NPP), k = i - vv * (2 * NPP);
+      zo[i] = zst[vv * (2 * NPP + 1) + k];
+    }
+    float* to = a.thrg + g0 * N4;
+    for (int i = tid; i < vce * N4; i += nth) {
+      const int vv = i / N4, k = i - vv * N4;
+      to[i] = tst[vv * (N4 + 1) + k];
+    }
   }
+  constexpr int NRB = (N + PREP_RB - 1) / PREP_RB;
   for (int vv = tid; vv < vce; vv += nth) {
-    const double2* yv = ys + vv * (m + 1);
-    double yn = 0.0, e2 = 0.0, zn = 0.0;
-    for (int r = 0; r < m; ++r) yn = fma(yv[r].x, yv[r].x, fma(yv[r].y, yv[r].y, yn));
-    for (int k = 0; k < N; ++k) { e2 += e2s[vv * N + k]; zn += zns[vv * N + k]; }
+    double e2 = 0.0, zn = 0.0;
+#pragma unroll
+    for (int w = 0; w < NRB; ++w) { e2 += e2s[w * PREP_VC + vv]; zn += zns[w * PREP_VC + vv]; }
+    const double yn = e2s[8 * PREP_VC + vv];
     a.vaux[g0 + vv] = make_float2((float)sqrt(e2) * 1.001f, (float)(yn - zn));
   }
 }
@@ -664,7 +673,7 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos) {
   const int64_t B = a.n_ch * a.V;
   const int64_t gv = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
   if (par >= npar || gv >= B) return;
-  const int c = (int)(gv / a.V);
+  const int c = (int)gv / (int)a.V;   // B < 2^31 (checked on the host)
   const float* tab = a.tables + (int64_t)c * TableLayout(a.m, N).total;
   const TabPtrs T = tab_ptrs(tab, a.m, N);
   const int p0 = par * tp.stride[pos + 1];
