@@ -75,16 +75,19 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
   for (int idx = tid; idx < n * n; idx += PLAN_THREADS) Rp[idx] = make_double2(0.0, 0.0);
   __syncthreads();
 
-  // Column bookkeeping, replicated identically in every warp: lane j owns
-  // physical column j (norm, logical position, chosen).
+  // Column bookkeeping in warp 0: lane j owns physical column j (downdated
+  // norm, logical position); the pivot and the chosen set are published
+  // through shared memory for the other warps.
+  __shared__ int piv_s;
+  __shared__ unsigned chosen_s;
   const bool own = lane < n;
   double norm = 0.0;
-  if (own)
+  if (w == 0 && own)
     for (int r = 0; r < ma; ++r) {
       double2 a = A[r * ns + lane];
       norm = fma(a.x, a.x, fma(a.y, a.y, norm));
     }
-  int logpos = lane;     // logical position of my physical column
+  int logpos = lane;     // logical position of my physical column (warp 0)
   bool chosen = !own;
   int my_final = -1;     // final logical position (== step at which chosen)
   // rows of this warp for the column updates
@@ -92,22 +95,27 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
   const int r0 = w * rb, r1 = min(ma, r0 + rb);
 
   for (int k = 0; k < n; ++k) {
-    // pivot: max downdated norm, ties -> smallest logical position (first max)
-    double bv = chosen ? -1.0 : norm;
-    int bp = chosen ? 0x7fffffff : logpos;
-    int bl = lane;
+    if (w == 0) {
+      // pivot: max downdated norm, ties -> smallest logical position (first max)
+      double bv = chosen ? -1.0 : norm;
+      int bp = chosen ? 0x7fffffff : logpos;
+      int bl = lane;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      int op = __shfl_xor_sync(0xffffffffu, bp, o);
-      int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bl = ol; }
+      for (int o = 16; o; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bl = ol; }
+      }
+      // exchange logical positions of column-at-k and the pivot column
+      if (!chosen && logpos == k) logpos = bp;
+      if (lane == bl) { logpos = k; chosen = true; my_final = k; }
+      const unsigned cm = __ballot_sync(0xffffffffu, chosen);
+      if (lane == 0) { piv_s = bl; chosen_s = cm; }
     }
-    const int cp = bl;                      // physical pivot column
-    const int cp_pos = bp;                  // its current logical position
-    // exchange logical positions of column-at-k and the pivot column
-    if (!chosen && logpos == k) logpos = cp_pos;
-    if (lane == cp) { logpos = k; chosen = true; my_final = k; }
+    __syncthreads();
+    const int cp = piv_s;                   // physical pivot column
+    const bool ch = (chosen_s >> lane) & 1u;
 
     // r_kk from the pivot column (thread per row, fixed-order block reduction)
     double part = 0.0;
@@ -118,10 +126,14 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     part = warp_sum_d(part);
     if (lane == 0) rkp[w] = part;
     __syncthreads();
-    double ss = 0.0;
+    double rkk = 0.0;
+    if (lane == 0) {   // one sqrt per warp (the MUFU/slow path is costly), then broadcast
+      double ss = 0.0;
 #pragma unroll
-    for (int i = 0; i < PLAN_WARPS; ++i) ss += rkp[i];
-    const double rkk = fmax(sqrt(ss), 1e-300);
+      for (int i = 0; i < PLAN_WARPS; ++i) ss += rkp[i];
+      rkk = fmax(sqrt(ss), 1e-300);
+    }
+    rkk = __shfl_sync(0xffffffffu, rkk, 0);
     if (tid < ma) {
       const double2 a = A[tid * ns + cp];
       A[tid * ns + cp] = make_double2(a.x / rkk, a.y / rkk);
@@ -130,7 +142,7 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     __syncthreads();
     // proj_j = q^H a_j over this warp's rows -> partials -> fixed-order sum
     double pr = 0.0, pi = 0.0;
-    if (!chosen) {
+    if (!ch) {
       double pr2 = 0.0, pi2 = 0.0;
       int r = r0;
       for (; r + 2 <= r1; r += 2) {
@@ -149,7 +161,7 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
       red[w * 32 + lane] = make_double2(pr + pr2, pi + pi2);
     }
     __syncthreads();
-    if (!chosen) {
+    if (!ch) {
       pr = 0.0;
       pi = 0.0;
 #pragma unroll
@@ -164,8 +176,10 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
       }
       norm = fmax(norm - (pr * pr + pi * pi), 0.0);
     }
-    __syncthreads();
+    // (no barrier here: the next step's pivot needs only warp 0's own norms,
+    // and its first barrier orders these updates before the next reads of A)
   }
+  __syncthreads();
 
   // ---- outputs in logical order ----
   __shared__ int phys_of[MPNL_MAX_N];

@@ -678,6 +678,7 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos) {
   const TabPtrs T = tab_ptrs(tab, a.m, N);
   const int p0 = par * tp.stride[pos + 1];
   uint8_t* vlist = a.lists + gv * tp.list_bytes;
+  const float thr_pos = __ldg(a.thrg + gv * N4 + pos);   // issued early (used by the guard)
   // acc of row pos after the expanded layers above it (the traversal's fma order)
   const float2 z = reinterpret_cast<const float2*>(a.zq + gv * NPP)[pos];
   float xr = z.x, xi = z.y;
@@ -692,20 +693,59 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos) {
     }
   }
   const float kx = T.lay4[pos].x;
-  const float Eb = 0.5f - a.thrg[gv * N4 + pos];   // index-domain centre error bound
+  const float Eb = 0.5f - thr_pos;   // index-domain centre error bound
   int ox[L], oy[L];
   float dx[L], dy[L];
   se_order<L>(__fmul_rn(xr, kx), ox, dx);
   se_order<L>(__fmul_rn(xi, kx), oy, dy);
-  int w[L];
-  float nk[L];
-#pragma unroll
-  for (int i = 0; i < L; ++i) { w[i] = 0; nk[i] = dx[i] + dy[0]; }
   constexpr int NW = (EMAX + 3) / 4;
   unsigned words[NW];
 #pragma unroll
   for (int i = 0; i < NW; ++i) words[i] = 0u;
   float kprev = 0.f, knext = 0.f;
+  if constexpr (EMAX <= 4) {
+    // E <= 4: the E + 1 smallest sums lie in row 0, column 0 or at (1,1)
+    // ((i+1)(j+1) <= 5): a two-pointer merge of row 0 and column 0 plus the corner
+    constexpr int K = (L - 1) < 4 ? (L - 1) : 4;
+    float ra[K], cb[K];
+    unsigned la[K], lb[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      ra[t] = dx[0] + dy[t + 1];
+      cb[t] = dx[t + 1] + dy[0];
+      la[t] = ((unsigned)ox[0] << 3) | (unsigned)oy[t + 1];
+      lb[t] = ((unsigned)ox[t + 1] << 3) | (unsigned)oy[0];
+    }
+    const float cc = dx[1] + dy[1];
+    const unsigned lc = ((unsigned)ox[1] << 3) | (unsigned)oy[1];
+    words[0] = ((unsigned)ox[0] << 3) | (unsigned)oy[0];
+    kprev = dx[0] + dy[0];
+    int i = 0, j = 0;
+    bool ct = false;
+#pragma unroll
+    for (int k = 1; k <= 4; ++k) {
+      if (k > E) break;
+      const float va = i < K ? dyn_at(ra, i) : INF;
+      const float vb = j < K ? dyn_at(cb, j) : INF;
+      const float vc = (i >= 1 && j >= 1 && !ct) ? cc : INF;
+      const bool ta = va <= vb && va <= vc, tb = !ta && vb <= vc;
+      const float v = ta ? va : (tb ? vb : vc);
+      if (k < E) {
+        const unsigned b = ta ? dyn_at(la, i) : (tb ? dyn_at(lb, j) : lc);
+        words[k >> 2] |= b << (8 * (k & 3));
+        kprev = v;
+      } else {
+        knext = v;
+      }
+      i += ta ? 1 : 0;
+      j += tb ? 1 : 0;
+      ct = ct || (!ta && !tb);
+    }
+  } else {
+  int w[L];
+  float nk[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) { w[i] = 0; nk[i] = dx[i] + dy[0]; }
   // L = 8: the per-axis orders live in per-thread (transposed) shared memory,
   // so the merge's data-dependent lookups are single LDS instead of select chains
   constexpr bool SMEM = L == 8;
@@ -752,6 +792,7 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos) {
     } else {
       knext = best;
     }
+  }
   }
   uint8_t* out = vlist + tp.list_off[pos] + par * E;
   if ((E & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
@@ -1055,22 +1096,38 @@ template <int N, int L>
 __global__ void __launch_bounds__(128)
 verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
   (void)unused;
+  constexpr int NPP = (N + 1) / 2;
+  constexpr int TW = N + N * NPP;   // float4 of (lay, rcol) per channel
   __shared__ TreeParams tp;
+  __shared__ float4 tabs[2][TW];    // the CTA's (at most two) channels' traversal tables
+  const int m = a.m;
+  const TableLayout tl(m, N);
+  const int64_t B = a.n_ch * a.V;
+  const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t c0 = g0 / a.V, c1 = min(g0 + (int64_t)blockDim.x, B) - 1;
+  const int nst = (c1 / a.V - c0) < 2 ? (int)(c1 / a.V - c0) + 1 : 0;   // staged channels
   {
     const int* s = reinterpret_cast<const int*>(&tparam);
     int* d = reinterpret_cast<int*>(&tp);
     for (int i = threadIdx.x; i < (int)(sizeof(TreeParams) / 4); i += blockDim.x) d[i] = s[i];
+    for (int i = threadIdx.x; i < nst * TW; i += blockDim.x) {
+      const int j = i / TW, o = i - j * TW;
+      tabs[j][o] = reinterpret_cast<const float4*>(a.tables + (c0 + j) * (int64_t)tl.total +
+                                                   tl.off_lay)[o];
+    }
   }
   __syncthreads();
-  const int m = a.m;
-  const TableLayout tl(m, N);
   const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
-  const int64_t B = a.n_ch * a.V;
-  constexpr int NPP = (N + 1) / 2;
-  const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gv = g0 + threadIdx.x;
   if (gv >= B) return;
   const int64_t c = gv / a.V;
-  const float* tab = a.tables + c * (int64_t)tl.total;
+  TabPtrs T;
+  if (c - c0 < nst) {
+    T.lay4 = tabs[c - c0];
+    T.rcol = reinterpret_cast<const float*>(tabs[c - c0] + N);
+  } else {
+    T = tab_ptrs(a.tables + c * (int64_t)tl.total, m, N);
+  }
   float4 zl[NPP];
 #pragma unroll
   for (int q = 0; q < NPP; ++q) zl[q] = a.zq[gv * NPP + q];
@@ -1079,7 +1136,14 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
   const int2 pth = a.vpath[gv];
   int lab[N];
   float pre[N];
-  retrace_inline<N, L>(tab, m, zl, vlist, tp, pth.x, 0, lab, pre);
+  {
+    const int vl[1] = {0}, pp[1] = {pth.x};
+    const int64_t gvl[1] = {0};
+    float pd[1], ep[1];
+    unsigned em[1];
+    traverse_paths<N, L, 1, false, true>(T, zl, nullptr, vlist, tp, 0, vl, gvl, pp, pd, em, ep,
+                                         lab, pre, 0);
+  }
   if (res.y - res.x <= ped_tol(res.x, res.w, N) + ped_tol(res.y, res.w, N)) {
     // near-tie of the two best paths: a three-way tie goes to the fp64 kernel,
     // a two-way tie is settled in fp64 by the check kernel (which may rewrite
