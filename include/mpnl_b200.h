@@ -87,6 +87,24 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64,
                            uint8_t* flags, void* workspace,
                            int64_t workspace_bytes, void* stream);
 
+/* Host-buffer drop-in for the reference's numpy call sites (cli.py:236-239):
+ * h (n_ch, m, n), y (n_ch, v_per_ch, m) and the outputs hard (n_ch*v_per_ch, n)
+ * uint8 / metric float32 live in HOST memory (pinned for asynchronous
+ * copies).  Uploads all channels and plans them in one launch, then detects
+ * chunk_channels channels at a time through two device slots, overlapping the
+ * upload of the next chunk's observations, the computation of the current one
+ * (on `stream`) and the download of the previous one.  Same
+ * results as mpnl_plan + mpnl_detect_hard on the whole batch.  The outputs
+ * are complete when `stream` reaches this point. */
+int64_t mpnl_host_workspace_bytes(int64_t n_ch, int64_t chunk_channels, int64_t v_per_ch,
+                                  int m, int n, int q, int h_is_f64, int y_is_f64,
+                                  const int64_t* expansions);
+int mpnl_detect_hard_host(const void* h, int h_is_f64, const void* y, int y_is_f64,
+                          int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
+                          const int64_t* expansions, double noise_var, uint8_t* hard,
+                          float* metric, int64_t chunk_channels, void* workspace,
+                          int64_t workspace_bytes, void* stream);
+
 /* Full candidate list (reference-compatible mpnl_detect_batch), fp64:
  * labels (B, P, n) uint8 in path order and stream order, metrics (B, P)
  * float64, best (B,) int64, B = n_ch * v_per_ch, P = prod(expansions). */

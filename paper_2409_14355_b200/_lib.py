@@ -31,6 +31,9 @@ _SIGS = {
                           _f64, _vp, _vp, _vp, _vp, _i64, _vp], _i32),
     "mpnl_detect_hard_stage": ([_i32, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32,
                                 _i32, _vp, _f64, _vp, _vp, _vp, _vp, _i64, _vp], _i32),
+    "mpnl_host_workspace_bytes": ([_i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp], _i64),
+    "mpnl_detect_hard_host": ([_vp, _i32, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _vp, _f64,
+                               _vp, _vp, _i64, _vp, _i64, _vp], _i32),
     "mpnl_detect_full": ([_vp, _vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _vp, _f64,
                           _vp, _vp, _vp, _vp], _i32),
     "mpnl_set_guard_scale": ([_f64], None),

@@ -448,6 +448,168 @@ int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64, con
 
 }  // extern "C"
 
+// ------------------------------------------------------------------------------------------
+// Host-buffer drop-in: h, y and the outputs in (pinned) host memory.  Channels are
+// processed in chunks through two device slots; three streams overlap the upload
+// of chunk k+1, the plan + detection of chunk k (caller's stream) and the download
+// of chunk k-1.  Results are identical to mpnl_plan + mpnl_detect_hard on the
+// whole batch (channels and vectors are independent).
+// ------------------------------------------------------------------------------------------
+namespace {
+
+struct HostSlot {   // one of the two per-chunk device slots
+  int64_t y, hard, metric, ws, total;
+  int64_t ws_bytes;
+  HostSlot(int64_t C, int64_t V, int m, int n, int yb, int list_bytes) {
+    auto up = [](int64_t x) { return (x + 255) & ~int64_t(255); };
+    int64_t o = 0;
+    y = o; o = up(o + C * V * m * yb);
+    hard = o; o = up(o + C * V * n);
+    metric = o; o = up(o + C * V * 4);
+    ws_bytes = Workspace(C * V, list_bytes, n).total;
+    ws = o; o = up(o + ws_bytes);
+    total = o;
+  }
+};
+
+struct HostPlan {   // the whole batch's channels and plans (planned once, up front)
+  int64_t h, perm, r64, qh64, tables, total;
+  HostPlan(int64_t n_ch, int m, int n, int hb) {
+    auto up = [](int64_t x) { return (x + 255) & ~int64_t(255); };
+    int64_t o = 0;
+    h = o; o = up(o + n_ch * m * n * hb);
+    perm = o; o = up(o + n_ch * n * 4);
+    r64 = o; o = up(o + n_ch * n * n * 16);
+    qh64 = o; o = up(o + n_ch * n * m * 16);
+    tables = o; o = up(o + n_ch * TableLayout(m, n).total * 4);
+    total = o;
+  }
+};
+
+#define HOST_SLOTS 3
+struct HostPipe {
+  bool init = false;
+  cudaStream_t up = nullptr, down = nullptr, cs[HOST_SLOTS];
+  cudaEvent_t in_ready[HOST_SLOTS], done[HOST_SLOTS], out_done[HOST_SLOTS], fin, planned;
+};
+thread_local HostPipe g_pipe;
+
+int pipe_init() {
+  if (g_pipe.init) return MPNL_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&g_pipe.up, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g_pipe.down, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_pipe.planned, cudaEventDisableTiming);
+  for (int i = 0; i < HOST_SLOTS && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithFlags(&g_pipe.cs[i], cudaStreamNonBlocking);
+    if (e != cudaSuccess) break;
+    e = cudaEventCreateWithFlags(&g_pipe.in_ready[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_pipe.done[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_pipe.out_done[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_pipe.fin, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(e, "pipeline streams");
+  g_pipe.init = true;
+  return MPNL_OK;
+}
+
+}  // namespace
+
+extern "C" int64_t mpnl_host_workspace_bytes(int64_t n_ch, int64_t chunk_channels,
+                                             int64_t v_per_ch, int m, int n, int q,
+                                             int h_is_f64, int y_is_f64,
+                                             const int64_t* expansions) {
+  const int L = levels_for(q);
+  if (!L || n < 1 || n > MPNL_MAX_N || chunk_channels < 1 || n_ch < 0) return -1;
+  TreeBuild tb = build_tree(n, L, expansions);
+  if (!tb.ok) return -1;
+  const HostSlot hs(std::min(chunk_channels, std::max<int64_t>(n_ch, 1)), v_per_ch, m, n,
+                    y_is_f64 ? 16 : 8, tb.tp.list_bytes);
+  return HostPlan(n_ch, m, n, h_is_f64 ? 16 : 8).total + HOST_SLOTS * hs.total;
+}
+
+extern "C" int mpnl_detect_hard_host(const void* h, int h_is_f64, const void* y, int y_is_f64,
+                                     int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
+                                     const int64_t* expansions, double noise_var, uint8_t* hard,
+                                     float* metric, int64_t chunk_channels, void* workspace,
+                                     int64_t workspace_bytes, void* stream) {
+  if (int rc = check_dims(m, n, q)) return rc;
+  if (n_ch < 0 || v_per_ch < 0) return fail(MPNL_EINVAL, "negative batch");
+  if (n_ch == 0 || v_per_ch == 0) return MPNL_OK;
+  if (chunk_channels < 1) return fail(MPNL_EINVAL, "chunk_channels must be >= 1");
+  const int L = levels_for(q);
+  TreeBuild tb = build_tree(n, L, expansions);
+  if (!tb.ok) return fail(MPNL_EINVAL, tb.err);
+  const int64_t C = std::min(chunk_channels, n_ch);
+  const int hb = h_is_f64 ? 16 : 8, yb = y_is_f64 ? 16 : 8;
+  const HostPlan hp(n_ch, m, n, hb);
+  const HostSlot hs(C, v_per_ch, m, n, yb, tb.tp.list_bytes);
+  if (workspace_bytes < hp.total + HOST_SLOTS * hs.total)
+    return fail(MPNL_EINVAL, "workspace too small");
+  if (int rc = pipe_init()) return rc;
+  cudaStream_t comp = (cudaStream_t)stream, up = g_pipe.up, down = g_pipe.down;
+  char* pb = reinterpret_cast<char*>(workspace);
+  char* base = pb + hp.total;
+  const int64_t tf = TableLayout(m, n).total;
+  cudaError_t e = cudaSuccess;
+  // the uploads must not start before work already queued on the caller's stream
+  e = cudaEventRecord(g_pipe.fin, comp);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(up, g_pipe.fin, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(down, g_pipe.fin, 0);
+  // all channels first (small), planned in one launch while the observations stream in
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pb + hp.h, h, n_ch * m * n * hb, cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess) e = cudaEventRecord(g_pipe.fin, up);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, g_pipe.fin, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline");
+  if (int rc = mpnl_plan(pb + hp.h, h_is_f64, n_ch, m, n, q, noise_var,
+                         reinterpret_cast<int32_t*>(pb + hp.perm), pb + hp.r64, pb + hp.qh64,
+                         reinterpret_cast<float*>(pb + hp.tables), comp))
+    return rc;
+  e = cudaEventRecord(g_pipe.planned, comp);
+  for (int i = 0; i < HOST_SLOTS && e == cudaSuccess; ++i)
+    e = cudaStreamWaitEvent(g_pipe.cs[i], g_pipe.planned, 0);
+  const int64_t K = (n_ch + C - 1) / C;
+  for (int64_t k = 0; k < K && e == cudaSuccess; ++k) {
+    const int sl = (int)(k % HOST_SLOTS);
+    cudaStream_t cst = g_pipe.cs[sl];   // one compute stream per slot: chunk tails overlap
+    char* sb = base + sl * hs.total;
+    const int64_t c0 = k * C, cn = std::min(C, n_ch - c0);
+    // upload (slot free once the compute of its previous chunk is done)
+    if (k >= HOST_SLOTS) e = cudaStreamWaitEvent(up, g_pipe.done[sl], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(sb + hs.y, (const char*)y + c0 * v_per_ch * m * yb,
+                          cn * v_per_ch * m * yb, cudaMemcpyHostToDevice, up);
+    if (e == cudaSuccess) e = cudaEventRecord(g_pipe.in_ready[sl], up);
+    // detect (outputs free once the slot's previous chunk is downloaded)
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cst, g_pipe.in_ready[sl], 0);
+    if (e == cudaSuccess && k >= HOST_SLOTS) e = cudaStreamWaitEvent(cst, g_pipe.out_done[sl], 0);
+    if (e != cudaSuccess) break;
+    const int rc = mpnl_detect_hard(
+        reinterpret_cast<int32_t*>(pb + hp.perm) + c0 * n,
+        reinterpret_cast<double2*>(pb + hp.r64) + c0 * n * n,
+        reinterpret_cast<double2*>(pb + hp.qh64) + c0 * n * m,
+        reinterpret_cast<float*>(pb + hp.tables) + c0 * tf, sb + hs.y, y_is_f64, cn, v_per_ch,
+        m, n, q, expansions, noise_var, reinterpret_cast<uint8_t*>(sb + hs.hard),
+        reinterpret_cast<float*>(sb + hs.metric), nullptr, sb + hs.ws, hs.ws_bytes, cst);
+    if (rc) return rc;
+    e = cudaEventRecord(g_pipe.done[sl], cst);
+    // download
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(down, g_pipe.done[sl], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hard + c0 * v_per_ch * n, sb + hs.hard, cn * v_per_ch * n,
+                          cudaMemcpyDeviceToHost, down);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(metric + c0 * v_per_ch, sb + hs.metric, cn * v_per_ch * 4,
+                          cudaMemcpyDeviceToHost, down);
+    if (e == cudaSuccess) e = cudaEventRecord(g_pipe.out_done[sl], down);
+  }
+  // the caller's stream completes after the last download
+  if (e == cudaSuccess) e = cudaEventRecord(g_pipe.fin, down);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, g_pipe.fin, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline");
+  return MPNL_OK;
+}
+
 // ---- FFMA throughput probe (roofline denominator) ----
 __global__ void ffma_probe_kernel(float* out, int iters) {
   float x0 = threadIdx.x * 1e-3f, x1 = x0 + 1.f, x2 = x0 + 2.f, x3 = x0 + 3.f;

@@ -208,8 +208,16 @@ __device__ __forceinline__ float row_bound(float ynorm, float2 zk, float4 lyk, i
 }
 
 // fp32 PED error bound from the L2 norm of the per-layer acc bounds
+// (sqrt.approx: <= 2 ulp below the true root; the 1 + 2^-19 factor makes it an
+// upper bound, and every kernel evaluates the identical instruction sequence)
+__device__ __forceinline__ float sqrt_up(float b) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+  return __fmul_ru(r, 1.0000020f);
+}
 __device__ __forceinline__ float ped_tol(float b, float eacc, int n) {
-  return 2.f * sqrtf(b) * eacc + eacc * eacc + 2.f * n * MPNL_U * b;
+  return __fadd_ru(__fadd_ru(__fmul_ru(__fmul_ru(2.f, sqrt_up(b)), eacc), __fmul_ru(eacc, eacc)),
+                   __fmul_ru(2.f * n * MPNL_U, b));
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -439,13 +447,15 @@ __device__ __forceinline__ bool tless(float a, unsigned pa, float b, unsigned pb
 }
 
 __device__ __forceinline__ void top3_insert(Top3& t, float m, unsigned p) {
-  if (tless(m, p, t.m1, t.p1)) {
-    t.m3 = t.m2; t.m2 = t.m1; t.p2 = t.p1; t.m1 = m; t.p1 = p;
-  } else if (tless(m, p, t.m2, t.p2)) {
-    t.m3 = t.m2; t.m2 = m; t.p2 = p;
-  } else {
-    t.m3 = fminf(t.m3, m);
-  }
+  // branch-free: (m1,p1) <= (m2,p2) <= (m3) in the (metric, path) order
+  const bool lt1 = tless(m, p, t.m1, t.p1), lt2 = tless(m, p, t.m2, t.p2);
+  t.m3 = lt2 ? t.m2 : fminf(t.m3, m);
+  const float m2 = lt1 ? t.m1 : (lt2 ? m : t.m2);
+  const unsigned p2 = lt1 ? t.p1 : (lt2 ? p : t.p2);
+  t.m2 = m2;
+  t.p2 = p2;
+  t.m1 = lt1 ? m : t.m1;
+  t.p1 = lt1 ? p : t.p1;
 }
 
 __device__ __forceinline__ void top3_pop(Top3& t) {
@@ -805,7 +815,7 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos) {
       if (k < E) out[k] = (uint8_t)(words[k >> 2] >> (8 * (k & 3)));
   }
   // cut guard: distance keys are within 2 sqrt2 E (sqrt k) + 2E^2 (+ rounding)
-  const float bound = 2.8284272f * Eb * (sqrtf(kprev) + sqrtf(knext)) + 4.f * Eb * Eb +
+  const float bound = 2.8284272f * Eb * (sqrt_up(kprev) + sqrt_up(knext)) + 4.f * Eb * Eb +
                       8.f * MPNL_U * (knext + 1.f);
   if (knext - kprev <= bound) log_event(a, make_int4(p0, pos, (int)gv, EV_CUT));
 }
@@ -849,6 +859,27 @@ template <int N>
 __device__ __forceinline__ void trav_prefetch(const DetectArgs& a, const TravSmem& so, float* buf,
                                               int gv0, int nv, int list_bytes, int lane) {
   constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
+  const int nl = list_bytes >> 4;
+  if (nv == 1 && NPP + N4 / 4 + nl < 32) {
+    // one 16-byte chunk per lane: z' rows | thresholds | lists; lane 31: (E_acc, corr)
+    const char* src;
+    float* dst;
+    if (lane < NPP) {
+      src = reinterpret_cast<const char*>(a.zq + (int64_t)gv0 * NPP + lane);
+      dst = buf + so.zs + 4 * lane;
+    } else if (lane < NPP + N4 / 4) {
+      src = reinterpret_cast<const char*>(a.thrg + (int64_t)gv0 * N4 + 4 * (lane - NPP));
+      dst = buf + so.thr + 4 * (lane - NPP);
+    } else {
+      src = reinterpret_cast<const char*>(a.lists + (int64_t)gv0 * list_bytes) +
+            16 * (lane - NPP - N4 / 4);
+      dst = buf + so.lst + 4 * (lane - NPP - N4 / 4);
+    }
+    if (lane < NPP + N4 / 4 + nl) cp_async16(dst, src);
+    if (lane == 31) cp_async8(buf + so.eac, a.vaux + gv0);
+    cp_async_commit();
+    return;
+  }
   const float4* zsrc = a.zq + (int64_t)gv0 * NPP;
   for (int i = lane; i < nv * NPP; i += 32) cp_async16(buf + so.zs + 4 * i, zsrc + i);
   const float* tsrc = a.thrg + (int64_t)gv0 * N4;
@@ -1002,11 +1033,11 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         traverse_paths<N, L, PT, true, false, !VPI>(T, zs, thr, lch, tp, lbytes, vl, gvl, pp, ped,
                                                     evm, evp, nullptr, nullptr, -1,
                                                     use_xs ? xs : nullptr);
-        if (!VPI) {   // the bound includes this batch's own best
-          float bm = INF;
+        if (!VPI) {   // running top-3; the event bound includes this batch's own best
 #pragma unroll
-          for (int t = 0; t < PT; ++t) bm = ok[t] ? fminf(bm, ped[t]) : bm;
-          wbest = fminf(wbest, __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(bm))));
+          for (int t = 0; t < PT; ++t)
+            if (ok[t]) top3_insert(run, ped[t], (unsigned)pp[t]);
+          wbest = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
         }
         // log paths with a marked decision whose prefix may still be competitive
 #pragma unroll
@@ -1022,9 +1053,6 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
           }
         }
         if (!VPI) {
-#pragma unroll
-          for (int t = 0; t < PT; ++t)
-            if (ok[t]) top3_insert(run, ped[t], (unsigned)pp[t]);
         } else if (P >= 32) {
           const int g = P >> 5;   // t-slots per vector
 #pragma unroll
@@ -1060,11 +1088,22 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         }
       }
       if (!VPI) {
-        float b1, b2, b3;
-        unsigned q1, q2;
-        warp_top3(run, b1, q1, b2, q2, b3);
+        // b1 = wbest; the 2nd path and the 3rd metric only matter for a near-tie
+        const unsigned k1 = __float_as_uint(wbest);
+        const unsigned q1 =
+            __reduce_min_sync(0xffffffffu, __float_as_uint(run.m1) == k1 ? run.p1 : 0xffffffffu);
+        if (__float_as_uint(run.m1) == k1 && run.p1 == q1) top3_pop(run);
+        const float b2 = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
+        unsigned q2 = 0xffffffffu;
+        float b3 = b2;
+        if (b2 - wbest <= ped_tol(wbest, weacc[0], N) + ped_tol(b2, weacc[0], N)) {
+          q2 = __reduce_min_sync(0xffffffffu,
+                                 __float_as_uint(run.m1) == __float_as_uint(b2) ? run.p1 : 0xffffffffu);
+          if (__float_as_uint(run.m1) == __float_as_uint(b2) && run.p1 == q2) top3_pop(run);
+          b3 = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
+        }
         if (lane == 0) {
-          a.vres[gbase] = make_float4(b1, b2, b3, weacc[0]);
+          a.vres[gbase] = make_float4(wbest, b2, b3, weacc[0]);
           a.vpath[gbase] = make_int2((int)q1, (int)q2);
         }
       }
@@ -1148,7 +1187,9 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
     // near-tie of the two best paths: a three-way tie goes to the fp64 kernel,
     // a two-way tie is settled in fp64 by the check kernel (which may rewrite
     // this vector's outputs with the second path)
-    if (res.z - res.x <= ped_tol(res.x, res.w, N) + ped_tol(res.z, res.w, N))
+    // (pth.y < 0: the traversal judged it no near-tie, a rounding-level
+    // disagreement of the two evaluations of the test -> fp64, conservatively)
+    if (pth.y < 0 || res.z - res.x <= ped_tol(res.x, res.w, N) + ped_tol(res.z, res.w, N))
       send_to_fp64(a, gv, 0);
     else
       log_event(a, make_int4(pth.x, pth.y, (int)gv, EV_TIE));

@@ -13,6 +13,8 @@ mpnl_plan_batch            detect.py:361-388 (+ _sorted_qr_batch)      K1 plan (
 mpnl_detect_batch          detect.py:473-488 (full candidate list)     K5 exact (fp64)
 mpnl_detect_hard           hard composition cli.py:236-239,            K3 fp32 traversal +
                            test_acceptance.py:114-117                  K5 fix-up of flags
+mpnl_hard_output           plan + hard composition from HOST arrays    K1-K5, pipelined
+                           (the cli._bench_chunk call, cli.py:236-239) host<->device copies
 mpnl_preprocess            detect.py:391-400                           K1
 mpnl_detect                detect.py:491-506                           K5
 detect("mpnl", ...)        detect.py:563-576                           K1 + K5
@@ -40,7 +42,7 @@ from .core import LLR_CLIP, Constellation, bits_from_labels
 
 __all__ = [
     "allocate_expansions", "BatchPathPlan", "PathPlan", "mpnl_plan_batch",
-    "mpnl_preprocess", "mpnl_detect_batch", "mpnl_detect_hard", "mpnl_detect",
+    "mpnl_preprocess", "mpnl_detect_batch", "mpnl_detect_hard", "mpnl_hard_output", "mpnl_detect",
     "detect", "DetectorInput", "CandidateList", "DetectionOutput",
     "llr_from_candidates", "DETECTOR_NAMES", "SingularChannelError",
 ]
@@ -258,6 +260,73 @@ def mpnl_detect_hard(plan: BatchPathPlan, h, y, c: Constellation, *, return_flag
         outs = [outs[0].cpu().numpy().astype(np.int64), outs[1].cpu().numpy().astype(np.float64)
                 ] + ([outs[2].cpu().numpy().astype(bool)] if return_flags else [])
     return tuple(outs)
+
+
+def _host_complex(a, name):
+    """-> (contiguous CPU complex tensor (pinned if it was a torch tensor), is_f64)."""
+    if isinstance(a, torch.Tensor):
+        t = a.detach()
+        if t.is_cuda:
+            raise ValueError(f"{name} must be a host array for mpnl_hard_output")
+        if t.dtype not in (torch.complex64, torch.complex128):
+            t = t.to(torch.complex128)
+        return t.contiguous(), t.dtype == torch.complex128
+    arr = np.asarray(a)
+    if arr.dtype != np.complex64:
+        arr = arr.astype(np.complex128)
+    return torch.from_numpy(np.ascontiguousarray(arr)), arr.dtype == np.complex128
+
+
+_HOST_WS: dict = {}
+
+
+def mpnl_hard_output(h, y, noise_var: float, n_paths: int, c: Constellation, *,
+                     chunk_channels: int | None = None, out=None):
+    """Plan + hard-output detection straight from HOST arrays, one call.
+
+    The reference's hard-output loop `mpnl_plan_batch` -> `mpnl_detect_batch`
+    -> `take_along_axis(labels, best)` (cli.py:236-239) with numpy inputs:
+    h (n_ch, M, N), y (n_ch, V, M) (one channel per resource block).  Runs
+    the C-ABI host pipeline (`mpnl_detect_hard_host`): uploads, kernels and
+    downloads of consecutive channel chunks overlap.  Pinned torch CPU
+    tensors give asynchronous copies.  Returns host (hard (n_ch, V, N) uint8
+    point labels in stream order, min_metric (n_ch, V) float32), complete on
+    return (the call synchronises the current stream)."""
+    lib = _lib.load()
+    ht, h64 = _host_complex(h, "h")
+    yt, y64 = _host_complex(y, "y")
+    if ht.dim() != 3 or yt.dim() != 3 or yt.shape[0] != ht.shape[0] or yt.shape[2] != ht.shape[1]:
+        raise ValueError("inconsistent channel/observation dimensions")
+    n_ch, m, n = ht.shape
+    v = yt.shape[1]
+    ex, _ = allocate_expansions(n, c.order, n_paths, max(0, n - m))
+    if chunk_channels is None:
+        # >= 4 chunks, <= ~12 MB of observations each: enough to overlap the
+        # transfers with the kernels, few enough that per-chunk latency stays small
+        ybytes = yt.numel() * yt.element_size()
+        chunks = max(4, -(-ybytes // (12 << 20)))
+        chunk_channels = max(1, -(-n_ch // chunks))
+    if out is None:
+        hard = torch.empty((n_ch, v, n), dtype=torch.uint8).pin_memory()
+        metric = torch.empty((n_ch, v), dtype=torch.float32).pin_memory()
+    else:
+        hard, metric = out
+    nb = int(lib.mpnl_host_workspace_bytes(n_ch, chunk_channels, v, m, n, c.order, int(h64),
+                                           int(y64), ex.ctypes.data))
+    if nb < 0:
+        raise ValueError("unsupported configuration")
+    dev = _device()
+    ws = _HOST_WS.get(dev)
+    if ws is None or ws.numel() < nb:
+        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+        _HOST_WS[dev] = ws
+    rc = lib.mpnl_detect_hard_host(ht.data_ptr(), int(h64), yt.data_ptr(), int(y64), n_ch, v, m,
+                                   n, c.order, ex.ctypes.data, float(noise_var), hard.data_ptr(),
+                                   metric.data_ptr(), chunk_channels, ws.data_ptr(), ws.numel(),
+                                   _stream())
+    _lib.check(rc, "mpnl_hard_output")
+    torch.cuda.current_stream().synchronize()
+    return hard, metric
 
 
 def mpnl_detect_batch(plan: BatchPathPlan, h, y, c: Constellation):

@@ -160,3 +160,38 @@ def test_noiseless_round_trip_full_size(name):
     hard, metric = det.mpnl_detect_hard(plan, h, y, c)
     assert torch.equal(hard.long().cpu(), torch.from_numpy(d["labels"]))
     assert float(metric.max()) < 1e-4
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5P64"])
+def test_host_pipeline_matches_reference_golden(name):
+    """The host-buffer drop-in (C-ABI mpnl_detect_hard_host) against the
+    reference goldens."""
+    import torch
+    det = _det()
+    g = np.load(GOLD / f"hard_{name}.npz")
+    cfg = CONFIGS[name]
+    c = constellation_for(cfg.order)
+    h = torch.from_numpy(np.ascontiguousarray(g["h"])).pin_memory()
+    y = torch.from_numpy(np.ascontiguousarray(g["y"])).pin_memory()
+    hard, metric = det.mpnl_hard_output(h, y, float(g["nv"]), cfg.n_paths, c, chunk_channels=1)
+    _check_hard(hard.numpy().astype(np.int64), metric.numpy().astype(np.float64), g["hard"],
+                g["m1"], g["m2"], f"{name} host pipeline")
+
+
+@pytest.mark.parametrize("name,n_rb,chunk", [("C2", 7, 2), ("C5P16", 5, 1), ("C3", 9, 4)])
+def test_host_pipeline_equals_device_path(name, n_rb, chunk):
+    """Chunked, three-stream pipelined host path == one-shot device path,
+    bit for bit (ragged last chunk, both device slots reused)."""
+    import torch
+    det = _det()
+    cfg = CONFIGS[name]
+    c = constellation_for(cfg.order)
+    d = generate(cfg, seed=77, n_rb=n_rb)
+    nv = float(d["nv"][0])
+    h = torch.from_numpy(d["h"]).pin_memory()
+    y = torch.from_numpy(d["y"]).pin_memory()
+    hard, metric = det.mpnl_hard_output(h, y, nv, cfg.n_paths, c, chunk_channels=chunk)
+    plan = det.mpnl_plan_batch(h.cuda(), nv, cfg.n_paths, c)
+    hd, md = det.mpnl_detect_hard(plan, h.cuda(), y.cuda(), c)
+    assert torch.equal(hd.cpu(), hard)
+    assert torch.equal(md.cpu(), metric)
