@@ -313,12 +313,19 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     if (e == cudaSuccess) e = cudaMemsetAsync(a.vflag, 0, 4 * B, st);
     if (e != cudaSuccess) return cuda_fail(e, "memset");
     if (slow) return MPNL_OK;
-    // per-vector preparation (z', guard thresholds), one warp per vector
+    // per-vector preparation (z', guard thresholds): CTA = vg x 32 vectors of a
+    // channel; the largest vg whose last chunk wastes <= 5% (and fits smem / 1024 threads)
     {
-      const int64_t pch = (v_per_ch + PREP_VC - 1) / PREP_VC;
+      int vg = 1;
+      for (int g = 4; g >= 2; g >>= 1) {
+        const int64_t vc = 32 * g, ch = (v_per_ch + vc - 1) / vc;
+        if (PrepSmem::threads(n, g) <= 1024 && PrepSmem(m, n, g).total <= 200 * 1024 &&
+            (double)v_per_ch >= 0.95 * (double)(ch * vc)) { vg = g; break; }
+      }
+      const int64_t vc = 32 * vg, pch = (v_per_ch + vc - 1) / vc;
       if (n_ch * pch > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
-      const PrepSmem ps(m, n);
-      e = launch_fast(n, L, 4, a, tp, (unsigned)(n_ch * pch), PrepSmem::threads(n), ps.total,
+      const PrepSmem ps(m, n, vg);
+      e = launch_fast(n, L, 4, a, tp, (unsigned)(n_ch * pch), PrepSmem::threads(n, vg), ps.total,
                       (int)pch, st);
     }
     if (e != cudaSuccess) return cuda_fail(e, "prep kernel");
@@ -326,7 +333,7 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
       if (tp.e[pos] == L * L) continue;
       const int npar = tp.n_paths / tp.stride[pos + 1];
       const int px = std::min(npar, 128), vy = std::max(1, 128 / px);
-      if ((B + vy - 1) / vy > 0x7fffffffLL || (npar + px - 1) / px > 65535)
+      if (n_ch * ((v_per_ch + vy - 1) / vy) > 0x7fffffffLL || (npar + px - 1) / px > 65535)
         return fail(MPNL_EUNSUPPORTED, "selection grid too large");
       e = launch_fast(n, L, 0, a, tp, 0, 128, 0, pos, st);
       if (e != cudaSuccess) return cuda_fail(e, "select kernel");

@@ -42,11 +42,11 @@ namespace mpnl {
 #define EX_LIST_MAX (48 * 1024)
 
 struct ExLayout {   // dynamic shared memory (bytes)
-  int tp, r, z, misc, perm, cand_m, cand_p, cand_k, lists, total;
+  int tp, r, rinv, qh, ys, z, misc, perm, cand_m, cand_p, cand_k, lists, total;
   int list_off[MPNL_MAX_N];
   bool listed[MPNL_MAX_N];
   int list_bytes;
-  __host__ __device__ ExLayout(const TreeParams& t, int n, int L, int exact_order) {
+  __host__ __device__ ExLayout(const TreeParams& t, int n, int L, int exact_order, int m = 0) {
     int lb = 0;
     for (int pos = n - 1; pos >= 0; --pos) {
       const int e = t.e[pos];
@@ -59,6 +59,9 @@ struct ExLayout {   // dynamic shared memory (bytes)
     tp = o; o += (int)sizeof(TreeParams);
     o = (o + 15) & ~15;
     r = o; o += 16 * n * n;
+    rinv = o; o += 16 * ((n + 1) / 2);   // (keeps the double2 arrays 16-byte aligned)
+    qh = o; o += 16 * n * m;
+    ys = o; o += 16 * m;
     z = o; o += 16 * n;
     misc = o; o += 32;
     perm = o; o += 4 * MPNL_MAX_N;
@@ -94,6 +97,20 @@ __device__ __forceinline__ int nearest_axis(double c) {
     if (d < bd || (d == bd && g < bg)) { bd = d; bg = g; bi = i; }
   }
   return bi;
+}
+
+// Fast path of nearest_axis for c = u / r: the level index coordinate
+// x = ((L-1) - c norm) / 2 from c ~ u * (1/r) (relative error ~1e-16), rounded.
+// When x is within 1e-9 of a half-integer (a decision boundary, including the
+// reference's distance ties) returns -1 and the caller takes the exact
+// division + nearest_axis path; elsewhere both give the same level.
+template <int L>
+__device__ __forceinline__ int nearest_fast(double c) {
+  const double x = 0.5 * ((double)(L - 1) - c * qam_norm_d(L));
+  if (!(fabs(x) < 1e6)) return -1;   // non-finite / degenerate r_pp: exact path
+  const double xr = rint(x);
+  if (0.5 - fabs(x - xr) < 1e-9) return -1;
+  return (int)fmin(fmax(xr, 0.0), (double)(L - 1));
 }
 
 template <int L>
@@ -141,14 +158,19 @@ static __device__ __noinline__ int ex_expanded_symbol(const TreeParams& tp, cons
 
 template <int N, int L>
 __global__ void __launch_bounds__(EX_THREADS)
-exact_kernel_t(const ExactArgs a, const TreeParams tparam) {
+exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
   extern __shared__ __align__(16) uint8_t exsm[];
   constexpr int Q = L * L;
   constexpr int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
   const int m = a.m;
-  const ExLayout lo(tparam, N, L, a.exact_order);
+  // fix-up mode usually has a handful of tasks: idle CTAs leave at once
+  const int64_t ntask = a.list ? (int64_t)(*a.count) : a.n_tasks;
+  if ((int64_t)blockIdx.x >= ntask) return;
   TreeParams& tp = *reinterpret_cast<TreeParams*>(exsm + lo.tp);
   double2* Rs = reinterpret_cast<double2*>(exsm + lo.r);
+  double2* QHs = reinterpret_cast<double2*>(exsm + lo.qh);
+  double* Rinv = reinterpret_cast<double*>(exsm + lo.rinv);
+  double2* Ys = reinterpret_cast<double2*>(exsm + lo.ys);
   double2* zs = reinterpret_cast<double2*>(exsm + lo.z);
   double* misc = reinterpret_cast<double*>(exsm + lo.misc);
   int* ps = reinterpret_cast<int*>(exsm + lo.perm);
@@ -163,7 +185,6 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam) {
     int* d = reinterpret_cast<int*>(&tp);
     for (int i = tid; i < (int)(sizeof(TreeParams) / 4); i += EX_THREADS) d[i] = s[i];
   }
-  const int64_t ntask = a.list ? (int64_t)(*a.count) : a.n_tasks;
   const int P = tparam.n_paths;
   int64_t cprev = -1;
   for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
@@ -174,10 +195,15 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam) {
     if (c != cprev) {
       const double2* R = a.r64 + c * (int64_t)N * N;
       for (int i = tid; i < N * N; i += EX_THREADS) Rs[i] = R[i];
-      if (tid < N) ps[tid] = a.perm[c * N + tid];
+      for (int i = tid; i < N * m; i += EX_THREADS) QHs[i] = QH[i];
+      if (tid < N) {
+        ps[tid] = a.perm[c * N + tid];
+        Rinv[tid] = 1.0 / R[tid * N + tid].x;
+      }
       cprev = c;
     }
-    auto yat = [&](int r, double& yr, double& yi) {
+    for (int r = tid; r < m; r += EX_THREADS) {
+      double yr, yi;
       if (a.y_f64) {
         const double2 v = reinterpret_cast<const double2*>(a.y)[gv * m + r];
         yr = v.x; yi = v.y;
@@ -185,6 +211,12 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam) {
         const float2 v = reinterpret_cast<const float2*>(a.y)[gv * m + r];
         yr = v.x; yi = v.y;
       }
+      Ys[r] = make_double2(yr, yi);
+    }
+    __syncthreads();
+    auto yat = [&](int r, double& yr, double& yi) {
+      yr = Ys[r].x;
+      yi = Ys[r].y;
     };
     // ---- 1. z = Q^H y ; c0 = ||y||^2 - ||z||^2 (M != N) ----
     if (tid < N) {
@@ -192,7 +224,7 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam) {
       for (int r = 0; r < m; ++r) {
         double yr, yi;
         yat(r, yr, yi);
-        const double2 q = QH[tid * m + r];
+        const double2 q = QHs[tid * m + r];
         zr = fma(q.x, yr, fma(-q.y, yi, zr));
         zi = fma(q.x, yi, fma(q.y, yr, zi));
       }
@@ -280,8 +312,11 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam) {
         const int e = tp.e[pos];
         int ir, ii;
         if (e == 1) {
-          ir = nearest_axis<L>(ur / rpp);
-          ii = nearest_axis<L>(ui / rpp);
+          const double ri = Rinv[pos];
+          ir = nearest_fast<L>(ur * ri);
+          ii = nearest_fast<L>(ui * ri);
+          if (ir < 0) ir = nearest_axis<L>(ur / rpp);
+          if (ii < 0) ii = nearest_axis<L>(ui / rpp);
         } else {
           const int b = ex_expanded_symbol<L>(tp, lo, lists, use_lists, a.exact_order, pos, p, ur,
                                               ui, rpp);
@@ -357,11 +392,11 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam) {
 
 template <int N, int L>
 cudaError_t launch_exact_t(const ExactArgs& a, const TreeParams& tp, int grid, cudaStream_t st) {
-  const ExLayout lo(tp, N, L, a.exact_order);
+  const ExLayout lo(tp, N, L, a.exact_order, a.m);
   const size_t smem = (size_t)lo.total;
   cudaFuncSetAttribute(exact_kernel_t<N, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  exact_kernel_t<N, L><<<grid, EX_THREADS, smem, st>>>(a, tp);
+  exact_kernel_t<N, L><<<grid, EX_THREADS, smem, st>>>(a, tp, lo);
   return cudaGetLastError();
 }
 

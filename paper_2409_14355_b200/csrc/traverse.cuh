@@ -499,43 +499,48 @@ __device__ __forceinline__ void group_top3(Top3 t, int width, float& b1, unsigne
 }
 
 // ===========================================================================
-// K1b: per-vector preparation.  CTA = a channel's chunk of PREP_VC = 32
-// vectors, lane = vector, warp = block of 4 rows: the channel's fp64 Q^H
-// (transposed) is read as warp-uniform broadcasts, each lane's y_r feeds 4
+// K1b: per-vector preparation.  CTA = a channel's chunk of vg x 32 vectors,
+// warp = (32-vector group, block of 4 rows), lane = vector: the channel's fp64
+// Q^H (transposed) is read as warp-uniform broadcasts, each lane's y_r feeds 4
 // rows.  z'_k = fl32((Q^H y)_k - shift_k) (fp64 rotation, one rounding), the
 // per-layer guard thresholds of the fp32 traversal, then per vector E_acc (L2
 // over layers) and the M > N metric offset (fixed-order sums).  Results are
 // staged in shared memory and written as contiguous rows.
 // ===========================================================================
-#define PREP_VC 32
 #define PREP_RB 4   // rows per warp
 
+// vg = 32-vector groups per CTA (CTA = vg * 32 vectors of one channel)
 struct PrepSmem {
-  int qt, sh, ly, y, z, th, e2, zn, total;   // bytes
-  __host__ __device__ PrepSmem(int m, int n) {
+  int vc, qt, sh, ly, y, z, th, e2, zn, total;   // bytes
+  __host__ __device__ PrepSmem(int m, int n, int vg) {
     const int npp = (n + 1) / 2, n4 = (n + 3) & ~3;
+    vc = 32 * vg;
     int o = 0;
     qt = o; o += 16 * m * n;
     sh = o; o += 16 * n;
     ly = o; o += 16 * n;
-    y = o; o += 16 * PREP_VC * (m + 1);        // padded rows (bank spread)
-    z = o; o += 8 * PREP_VC * (2 * npp + 1);   // staged z' rows (float2, padded stride)
-    th = o; o += 4 * PREP_VC * (n4 + 1);       // staged thresholds (padded stride)
-    e2 = o; o += 8 * PREP_VC * 9;              // per (row block, vector) partial sums; [8]: ||y||^2
-    zn = o; o += 8 * PREP_VC * 8;
+    y = o; o += 16 * vc * (m + 1);        // padded rows (bank spread)
+    z = o; o += 8 * vc * (2 * npp + 1);   // staged z' rows (float2, padded stride)
+    th = o; o += 4 * vc * (n4 + 1);       // staged thresholds (padded stride)
+    e2 = o; o += 8 * vc * 9;              // per (row block, vector) partial sums; [8]: ||y||^2
+    zn = o; o += 8 * vc * 8;
     total = o;
   }
-  __host__ __device__ static int threads(int n) { return 32 * ((n + PREP_RB - 1) / PREP_RB); }
+  __host__ __device__ static int nrb(int n) { return (n + PREP_RB - 1) / PREP_RB; }
+  __host__ __device__ static int threads(int n, int vg) { return 32 * vg * nrb(n); }
 };
 
 template <int N, int L>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
   (void)tparam;
   constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
+  constexpr int NRB = (N + PREP_RB - 1) / PREP_RB;
   extern __shared__ __align__(16) uint8_t psm[];
   const int m = a.m;
-  const PrepSmem so(m, N);
+  const int vg = blockDim.x / (32 * NRB);
+  const PrepSmem so(m, N, vg);
+  const int VC = so.vc;
   double2* qt = reinterpret_cast<double2*>(psm + so.qt);
   double2* sh = reinterpret_cast<double2*>(psm + so.sh);
   float4* ly = reinterpret_cast<float4*>(psm + so.ly);
@@ -546,8 +551,8 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
   double* zns = reinterpret_cast<double*>(psm + so.zn);
   const TableLayout tl(m, N);
   const int64_t c = blockIdx.x / chunks;
-  const int v0 = (blockIdx.x % chunks) * PREP_VC;
-  const int vce = (int)min((int64_t)PREP_VC, a.V - v0);
+  const int v0 = (blockIdx.x % chunks) * VC;
+  const int vce = (int)min((int64_t)VC, a.V - v0);
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5;
   const float* tab = a.tables + c * (int64_t)tl.total;
@@ -558,8 +563,10 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
     const double2* s2 = reinterpret_cast<const double2*>(tab + tl.off_shift);
     const float4* l4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
     for (int i = tid; i < N; i += nth) { sh[i] = s2[i]; ly[i] = l4[i]; }
+    // flat copy; (v, r) by a float reciprocal (exact for i < 2^13: v*m + r <= 128*64)
+    const float rm = 1.f / (float)m;
     for (int i = tid; i < vce * m; i += nth) {
-      const int v = i / m, r = i - v * m;
+      const int v = (int)(((float)i + 0.5f) * rm), r = i - v * m;
       double2 yv;
       if (a.y_f64) {
         yv = reinterpret_cast<const double2*>(a.y)[g0 * m + i];
@@ -571,8 +578,10 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
     }
   }
   __syncthreads();
-  const int v = lane;
-  const int k0 = warp * PREP_RB;
+  // warp = (vector group, row block); lane = vector
+  const int rb = warp % NRB;
+  const int v = (warp / NRB) * 32 + lane;
+  const int k0 = rb * PREP_RB;
   if (v < vce) {
     const double2* yv = ys + v * (m + 1);
     double zr[PREP_RB], zi[PREP_RB];
@@ -608,30 +617,26 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
         znp += zr[j] * zr[j] + zi[j] * zi[j];
       }
     }
-    e2s[warp * PREP_VC + v] = e2p;
-    zns[warp * PREP_VC + v] = znp;
-    if (warp == 0) e2s[8 * PREP_VC + v] = yn;
+    e2s[rb * VC + v] = e2p;
+    zns[rb * VC + v] = znp;
+    if (rb == 0) e2s[8 * VC + v] = yn;
   }
   __syncthreads();
   // contiguous write-out of the chunk's rows (un-padding the staged strides)
   {
     float2* zo = reinterpret_cast<float2*>(a.zq + g0 * NPP);
-    for (int i = tid; i < vce * 2 * NPP; i += nth) {
-      const int vv = i / (2 * NPP), k = i - vv * (2 * NPP);
-      zo[i] = zst[vv * (2 * NPP + 1) + k];
-    }
     float* to = a.thrg + g0 * N4;
-    for (int i = tid; i < vce * N4; i += nth) {
-      const int vv = i / N4, k = i - vv * N4;
-      to[i] = tst[vv * (N4 + 1) + k];
+    const int nwarps = nth >> 5;
+    for (int vv = warp; vv < vce; vv += nwarps) {
+      if (lane < 2 * NPP) zo[vv * 2 * NPP + lane] = zst[vv * (2 * NPP + 1) + lane];
+      if (lane < N4) to[vv * N4 + lane] = tst[vv * (N4 + 1) + lane];
     }
   }
-  constexpr int NRB = (N + PREP_RB - 1) / PREP_RB;
   for (int vv = tid; vv < vce; vv += nth) {
     double e2 = 0.0, zn = 0.0;
 #pragma unroll
-    for (int w = 0; w < NRB; ++w) { e2 += e2s[w * PREP_VC + vv]; zn += zns[w * PREP_VC + vv]; }
-    const double yn = e2s[8 * PREP_VC + vv];
+    for (int w = 0; w < NRB; ++w) { e2 += e2s[w * VC + vv]; zn += zns[w * VC + vv]; }
+    const double yn = e2s[8 * VC + vv];
     a.vaux[g0 + vv] = make_float2((float)sqrt(e2) * 1.001f, (float)(yn - zn));
   }
 }
@@ -673,17 +678,17 @@ __device__ __forceinline__ void se_order(float x, int (&lev)[L], float (&d)[L]) 
 
 template <int N, int L, int EMAX>
 __global__ void __launch_bounds__(128)
-select_kernel(const DetectArgs a, const TreeParams tp, int pos) {
+select_kernel(const DetectArgs a, const TreeParams tp, int pos, int npar, int vblocks) {
   const int E = tp.e[pos];   // <= EMAX
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
   constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
   const float INF = __int_as_float(0x7f800000);
-  const int npar = tp.n_paths / tp.stride[pos + 1];
+  // grid.x = channel x vector block, grid.y = parent block: no per-thread division
+  const int c = blockIdx.x / vblocks;
+  const int vi = (blockIdx.x - c * vblocks) * blockDim.y + threadIdx.y;
   const int par = blockIdx.y * blockDim.x + threadIdx.x;
-  const int64_t B = a.n_ch * a.V;
-  const int64_t gv = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
-  if (par >= npar || gv >= B) return;
-  const int c = (int)gv / (int)a.V;   // B < 2^31 (checked on the host)
+  if (par >= npar || vi >= a.V) return;
+  const int64_t gv = (int64_t)c * a.V + vi;
   const float* tab = a.tables + (int64_t)c * TableLayout(a.m, N).total;
   const TabPtrs T = tab_ptrs(tab, a.m, N);
   const int p0 = par * tp.stride[pos + 1];

@@ -20,17 +20,17 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
     const int pos = extra, e = tp.e[pos];
     const int npar = tp.n_paths / tp.stride[pos + 1];
     const int px = std::min(npar, 128), vy = std::max(1, 128 / px);
-    const int64_t B = a.n_ch * a.V;
-    const dim3 blk(px, vy), grd((unsigned)((B + vy - 1) / vy), (unsigned)((npar + px - 1) / px));
+    const int vblocks = (int)((a.V + vy - 1) / vy);
+    const dim3 blk(px, vy), grd((unsigned)(a.n_ch * vblocks), (unsigned)((npar + px - 1) / px));
     if constexpr (L == 2) {
-      select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos);
+      select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos, npar, vblocks);
     } else if constexpr (L == 4) {
-      if (e <= 4) select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos);
-      else select_kernel<NN, L, 16><<<grd, blk, 0, st>>>(a, tp, pos);
+      if (e <= 4) select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos, npar, vblocks);
+      else select_kernel<NN, L, 16><<<grd, blk, 0, st>>>(a, tp, pos, npar, vblocks);
     } else {
-      if (e <= 4) select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos);
-      else if (e <= 16) select_kernel<NN, L, 16><<<grd, blk, 0, st>>>(a, tp, pos);
-      else select_kernel<NN, L, 64><<<grd, blk, 0, st>>>(a, tp, pos);
+      if (e <= 4) select_kernel<NN, L, 4><<<grd, blk, 0, st>>>(a, tp, pos, npar, vblocks);
+      else if (e <= 16) select_kernel<NN, L, 16><<<grd, blk, 0, st>>>(a, tp, pos, npar, vblocks);
+      else select_kernel<NN, L, 64><<<grd, blk, 0, st>>>(a, tp, pos, npar, vblocks);
     }
   } else if (kind == 1) {
     // persistent: grid = resident capacity (capped by the item count `extra`)
