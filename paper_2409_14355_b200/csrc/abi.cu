@@ -182,7 +182,7 @@ struct Workspace {
     lists = o; o = up(o + B * (int64_t)list_bytes);
     zq = o; o = up(o + B * 16 * (int64_t)((n + 1) / 2));
     thrg = o; o = up(o + B * 4 * (int64_t)((n + 3) & ~3));
-    vaux = o; o = up(o + B * 8);
+    vaux = o; o = up(o + B * 8 + 16);   // +16: the traversal's aligned bulk-copy window
     total = o;
   }
 };

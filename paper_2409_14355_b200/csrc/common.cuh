@@ -24,7 +24,7 @@ struct TableLayout {
   int m, n;
   int off_qh;     // M x N double2 : Q^H transposed (fp64): qhT[r][k], for z = Q^H y
   int off_shift;  // N double2     : constant symbol offset folded into z (fp64)
-  int off_lay;    // N float4      : per layer (kx = -1/c2r, c2r, S_k, |shift_k|)
+  int off_lay;    // N float4      : per layer (kx = -1/c2r, c2r, S_k, kxs = kx/(L-1))
   int off_rcol;   // N columns x NPP float4: column pos, row pair q holds
                   // {rr_2q, ri_2q, rr_2q+1, ri_2q+1} of r''[k][pos] (0 for k >= pos)
   int npp;        // row pairs, (N+1)/2

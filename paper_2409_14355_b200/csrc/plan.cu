@@ -239,9 +239,10 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
     float* ly = tc + tl.off_lay + 4 * k;
     ly[0] = (float)(-1.0 / c2r);   // kx: acc -> level-index units
     ly[1] = (float)c2r;
-    // guard inputs: S_k = sum_{j>k} |Re r''| + |Im r''| (as stored) and |shift_k|
+    // guard input S_k = sum_{j>k} |Re r''| + |Im r''| (as stored)
     ly[2] = (float)(sabs * (1.0 + 1e-6));
-    ly[3] = (float)(fmax(fabs(shr), fabs(shi)) * (1.0 + 1e-6));
+    // kxs: acc -> saturated slicing domain [0, 1] (level index / (L - 1))
+    ly[3] = (float)(-1.0 / (c2r * (double)(L - 1)));
   }
 }
 

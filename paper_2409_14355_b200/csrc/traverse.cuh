@@ -98,16 +98,20 @@ __device__ __forceinline__ void expanded_symbol(const TreeParams& tp, int pos, i
   }
 }
 
-// slice one axis: x = acc * kx (level-index units, kx = -1/c2r), n = round(x)
-// by the 1.5 * 2^23 magic number (exact for |x| < 2^22), t = x - n, symbol =
-// clamp(n, 0, L-1).  The packed twin in traverse_paths performs the very same
-// per-element operations (fma, sub, fma, min, max), so both are bit-identical.
+// slice one axis (kxs = -1/(c2r (L-1)), the saturated scale): s = sat(acc kxs)
+// in [0, 1], so n = round(s (L-1)) (1.5 * 2^23 magic number, exact) is the
+// nearest level index already clamped to [0, L-1], t = s (L-1) - n.  Returns
+// -n (the traversal carries negated level indices: a decision is then one
+// FMUL.SAT per axis + FFMA2 + FADD2, with no min/max clamping).  The packed
+// twin in traverse_paths performs the very same per-element operations, so
+// both are bit-identical.
 template <int L>
-__device__ __forceinline__ float slice_axis(float acc, float kx, float& t) {
-  const float mm = __fmaf_rn(acc, kx, MPNL_MAGIC);
+__device__ __forceinline__ float slice_axis(float acc, float kxs, float& t) {
+  const float s = __saturatef(__fmul_rn(acc, kxs));
+  const float mm = __fmaf_rn(s, (float)(L - 1), MPNL_MAGIC);
   const float nf = __fsub_rn(MPNL_MAGIC, mm);   // -n
-  t = __fmaf_rn(acc, kx, nf);
-  return fmaxf(fminf(-nf, (float)(L - 1)), 0.f);
+  t = __fmaf_rn(s, (float)(L - 1), nf);
+  return nf;
 }
 
 __device__ __forceinline__ float ped_step(float ped, float c2r, float fr, float fi, float ur,
@@ -245,13 +249,27 @@ __device__ __forceinline__ TabPtrs tab_ptrs(const float* tab, int m, int n) {
   return t;
 }
 
+// guard bookkeeping as two predicated instructions (no branch, no selects):
+// if (d > th) { evm |= bit; evp = min(evp, pre); }
+__device__ __forceinline__ void guard_mark(float d, float th, unsigned bit, float pre,
+                                           unsigned& evm, float& evp) {
+  asm("{\n\t.reg .pred p;\n\tsetp.gt.f32 p, %2, %3;\n\t@p or.b32 %0, %0, %4;\n\t"
+      "@p min.f32 %1, %1, %5;\n\t}"
+      : "+r"(evm), "+f"(evp)
+      : "f"(d), "f"(th), "r"(bit), "f"(pre));
+}
+
 // K3 inner loop: NS independent paths.  Per path: PED, mask of layers whose
-// decision was within the bound, PED prefix at the first such layer.
-// Accumulators are per row (re, im) f32x2 registers.  Slicing, the PED step
-// and the interference update are all packed: the update of row k is
-//   acc_k = FFMA2(rr_k (bcast), f, acc_k);  acc_k = FFMA2(-f.swap (lo only), ri_k (bcast), acc_k)
+// decision was within the bound, and a lower bound of the PED prefix at the
+// first such layer (the re-part partial sum, taken with a predicated min).
+// Accumulators are per row (re, im) f32x2 registers; decided symbols are held
+// as NEGATED level indices g = -n (what the magic-number rounding yields for
+// free), so every product with g uses a negated table operand -- exact, hence
+// bit-identical to the positive-form scalar twins (acc_step, warp_retrace).
+// The update of row k is
+//   acc_k = FFMA2(-rr_k (bcast), g, acc_k);  acc_k = FFMA2((-gi, gr), -ri_k (bcast), acc_k)
 // i.e. per element exactly acc_step's fma sequence, with no register moves
-// (the swap and the partial negation are free FFMA2 operand modifiers).
+// (swap, partial and broadcast negations are free FFMA2 operand modifiers).
 // One 128-bit LDS of r'' ({rr_2q, ri_2q, rr_2q+1, ri_2q+1}) feeds 4 FFMA2 per path.
 // zs: per vector NPP float4 {re_2q, im_2q, re_2q+1, im_2q+1}.
 // LAB (NS == 1): record level indices lab[pos] and PED prefix pre[pos] and
@@ -270,7 +288,7 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
   constexpr int N4 = (N + 3) & ~3;
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
   const float INF = __int_as_float(0x7f800000);
-  u64 acc[NS][2 * NPP], ped2[NS], evp2[NS];
+  u64 acc[NS][2 * NPP], ped2[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
 #pragma unroll
@@ -281,29 +299,30 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
     }
     ped2[s] = 0ull;
     evm[s] = 0u;
-    evp2[s] = pk2(INF, INF);
+    evp[s] = INF;
   }
   const int top_lo = N - tp.n_top;   // layers pos >= top_lo are expanded (n_top <= XM)
   const float4* rc4 = reinterpret_cast<const float4*>(T.rcol);
   const u64 MAGIC2 = pk2(MPNL_MAGIC, MPNL_MAGIC);
+  const u64 LM2 = pk2((float)(L - 1), (float)(L - 1));
 #pragma unroll
   for (int pos = N - 1; pos >= 0; --pos) {
     const float4 ly = T.lay4[pos];
-    const float kx = ly.x, c2r = ly.y;
-    u64 f2[NS];
+    const float kxs = ly.w, c2r = ly.y;
+    u64 g2[NS];   // negated level indices (-ir, -ii)
     if (pos >= N - XM && pos >= top_lo) {
       if (xs != nullptr) {
-        // per-lane precomputed symbols (paths fixed per lane): a float pair for
-        // a full layer, the list index for a partial one
+        // per-lane precomputed symbols (paths fixed per lane): a negated float
+        // pair for a full layer, the list index for a partial one
         const bool full = tp.e[pos] == L * L;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           const u64 x = xs[((N - 1 - pos) * NS + s) * MPNL_XS_STRIDE];
           if (full) {
-            f2[s] = x;
+            g2[s] = x;
           } else {
             const unsigned b = lists[(SAMEV ? 0 : (int)gvl[s]) * list_bytes + (int)(unsigned)x];
-            f2[s] = pk2((float)(b >> 3), (float)(b & 7u));
+            g2[s] = pk2(-(float)(b >> 3), -(float)(b & 7u));
           }
         }
       } else {
@@ -311,36 +330,33 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
         for (int s = 0; s < NS; ++s) {
           int ir, ii;
           expanded_symbol<L>(tp, pos, p[s], lists + gvl[s] * list_bytes, ir, ii);
-          f2[s] = pk2((float)ir, (float)ii);
+          g2[s] = pk2(-(float)ir, -(float)ii);
         }
       }
     } else {
       // packed slicing of (re, im): the per-element twin of slice_axis
-      const u64 kx2 = pk2(kx, kx);
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const u64 mm = ffma2(acc[s][pos], kx2, MAGIC2);
-        const u64 nf = fsub2(MAGIC2, mm);
-        f2[s] = pk2(fmaxf(fminf(-lo32(nf), (float)(L - 1)), 0.f),
-                    fmaxf(fminf(-hi32(nf), (float)(L - 1)), 0.f));
+        const u64 s2 = pk2(__saturatef(__fmul_rn(lo32(acc[s][pos]), kxs)),
+                           __saturatef(__fmul_rn(hi32(acc[s][pos]), kxs)));
+        const u64 mm = ffma2(s2, LM2, MAGIC2);
+        g2[s] = fsub2(MAGIC2, mm);
         if (GUARD) {
-          const u64 t2 = ffma2(acc[s][pos], kx2, nf);
+          const u64 t2 = ffma2(s2, LM2, g2[s]);
           const float th = thr[(SAMEV ? 0 : vl[s]) * N4 + pos];
-          const bool near = fmaxf(fabsf(lo32(t2)), fabsf(hi32(t2))) > th;
-          const bool first = near && evm[s] == 0u;
-          evm[s] |= near ? (1u << pos) : 0u;
-          evp2[s] = first ? ped2[s] : evp2[s];
+          guard_mark(fmaxf(fabsf(lo32(t2)), fabsf(hi32(t2))), th, 1u << pos, lo32(ped2[s]),
+                     evm[s], evp[s]);
         }
       }
     }
     if (LAB) {
-      lab[pos] = (int)lo32(f2[0]) * 8 + (int)hi32(f2[0]);
+      lab[pos] = (int)(-lo32(g2[0])) * 8 + (int)(-hi32(g2[0]));
       pre[pos] = lo32(ped2[0]) + hi32(ped2[0]);
       if (pos == stop) return;
     }
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      const u64 e2 = ffma2(pk2(c2r, c2r), f2[s], acc[s][pos]);   // c2r f + u
+      const u64 e2 = ffma2(pk2(-c2r, -c2r), g2[s], acc[s][pos]);   // c2r n + u
       ped2[s] = ffma2(e2, e2, ped2[s]);
     }
     // push this layer's symbols into the rows below: acc_k += r''_k,pos * s
@@ -350,21 +366,18 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
       const float4 r = rc[q];              // {rr_2q, ri_2q, rr_2q+1, ri_2q+1}
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const u64 fs = pk2(-hi32(f2[s]), lo32(f2[s]));   // (-fi, fr): operand modifiers
-        acc[s][2 * q] = ffma2(pk2(r.x, r.x), f2[s], acc[s][2 * q]);
-        acc[s][2 * q] = ffma2(fs, pk2(r.y, r.y), acc[s][2 * q]);
+        const u64 gs = pk2(-hi32(g2[s]), lo32(g2[s]));   // (fi, -fr): operand modifiers
+        acc[s][2 * q] = ffma2(pk2(-r.x, -r.x), g2[s], acc[s][2 * q]);
+        acc[s][2 * q] = ffma2(gs, pk2(-r.y, -r.y), acc[s][2 * q]);
         if (2 * q + 1 < pos) {
-          acc[s][2 * q + 1] = ffma2(pk2(r.z, r.z), f2[s], acc[s][2 * q + 1]);
-          acc[s][2 * q + 1] = ffma2(fs, pk2(r.w, r.w), acc[s][2 * q + 1]);
+          acc[s][2 * q + 1] = ffma2(pk2(-r.z, -r.z), g2[s], acc[s][2 * q + 1]);
+          acc[s][2 * q + 1] = ffma2(gs, pk2(-r.w, -r.w), acc[s][2 * q + 1]);
         }
       }
     }
   }
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    ped[s] = lo32(ped2[s]) + hi32(ped2[s]);
-    evp[s] = lo32(evp2[s]) + hi32(evp2[s]);
-  }
+  for (int s = 0; s < NS; ++s) ped[s] = lo32(ped2[s]) + hi32(ped2[s]);
 }
 
 // Single-path re-trace with the identical arithmetic: level indices lab[pos]
@@ -612,7 +625,7 @@ prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
         zst[v * (2 * NPP + 1) + k] = z;   // (re, im) per row
         const float4 lk = ly[k];
         const float e = row_bound(ynf, z, lk, k, m, N, L, a.guard_scale, 0);
-        tst[v * (N4 + 1) + k] = 0.5f - e / lk.y - MPNL_U * 2.f * L;
+        tst[v * (N4 + 1) + k] = 0.5f - e / lk.y - MPNL_U * 3.f * L;
         e2p += (double)e * e;
         znp += zr[j] * zr[j] + zi[j] * zi[j];
       }
@@ -833,25 +846,41 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos, int npar, int vb
 // so static ranges are balanced).  An item is one vector (or, when P < 32 PT,
 // `vpi` vectors of the same channel).  The range is walked channel segment by
 // channel segment: the channel's tables are staged in shared memory once per
-// segment, and each warp walks its items with the next item's z' rows, guard
-// thresholds, E_acc and selection lists prefetched by cp.async into a
-// per-warp double buffer, so the global latency hides behind the traversal.
+// segment; each warp owns a balanced sub-range of the segment and walks it in
+// chunks of consecutive vectors.  A chunk's z' rows, guard thresholds,
+// selection lists and (E_acc, corr) are contiguous in the workspace, so one
+// lane fetches the next chunk with four TMA bulk copies (cp.async.bulk,
+// completion on a per-buffer mbarrier) into the warp's second buffer while the
+// warp traverses the current one.
 // ===========================================================================
+#ifndef MPNL_CHUNK_V
+#define MPNL_CHUNK_V 8          // vectors per warp chunk (one bulk-copy group)
+#endif
 struct TravSmem {
-  int tpo, tab, wbuf, bufsz, zs, thr, eac, lst, xs, ev, evn, total_bytes;   // floats / bytes
+  int tpo, tab, wbuf, bufsz, zs, thr, lst, eac, mbar, xs, ev, evn, total_bytes;   // floats / bytes
+  int ck, cv;   // items and vectors per chunk
   __host__ __device__ TravSmem(int m, int n, int warps, int nvi, int list_bytes) {
     TableLayout tl(m, n);
     const int npp = (n + 1) / 2, n4 = (n + 3) & ~3;
-    // per-warp buffer (floats): z' row pairs | thresholds | (E_acc, corr) | lists
+    // chunk: up to MPNL_CHUNK_V vectors, at most ~2 KB per buffer (large
+    // selection lists -> fewer vectors per chunk; occupancy is kept)
+    const int bv = 16 * npp + 4 * n4 + list_bytes + 8;
+    ck = MPNL_CHUNK_V / nvi;
+    if (ck * nvi * bv > 2048) ck = 2048 / (nvi * bv);
+    if (ck < 1) ck = 1;
+    cv = ck * nvi;
+    // per-warp chunk buffer (floats): z' row pairs | thresholds | lists |
+    // (E_acc, corr) pairs from the even vector at or below the chunk start
     zs = 0;
-    thr = zs + 4 * nvi * npp;
-    eac = thr + nvi * n4;
-    lst = eac + TableLayout::up4(2 * nvi);
-    bufsz = lst + nvi * list_bytes / 4;
+    thr = zs + 4 * cv * npp;
+    lst = thr + cv * n4;
+    eac = lst + cv * list_bytes / 4;
+    bufsz = eac + TableLayout::up4(2 * (cv + 2));
     int o = 0;
     tpo = o; o += TableLayout::up4((int)(sizeof(TreeParams) / 4));
     tab = o; o += tl.total;
     wbuf = o; o += warps * 2 * bufsz;
+    mbar = o; o += warps * 2 * 2;                  // u64 mbarrier per warp buffer
     xs = o; o += 2 * MPNL_XMAX * MPNL_PT_SMALL * MPNL_XS_STRIDE;   // u64 per-thread symbols
     ev = o; o += 4 * TRAV_EV_CAP;                  // int4 event buffer
     evn = o; o += 4;
@@ -859,43 +888,46 @@ struct TravSmem {
   }
 };
 
-// prefetch item (vectors gv0 .. gv0+nv-1) into the warp buffer `buf`
+// ---- TMA bulk copies (cp.async.bulk, completion on an mbarrier) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(void* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// issue the bulk copies of vectors gv0 .. gv0+nv-1 into the warp buffer `buf`
+// (lane 0 only; the buffer's previous contents must be consumed).  Every
+// source block is contiguous and 16-byte aligned; the (E_acc, corr) pairs are
+// fetched from the even vector at or below gv0 (workspace padded for it).
 template <int N>
-__device__ __forceinline__ void trav_prefetch(const DetectArgs& a, const TravSmem& so, float* buf,
-                                              int gv0, int nv, int list_bytes, int lane) {
+__device__ __forceinline__ void trav_issue(const DetectArgs& a, const TravSmem& so, float* buf,
+                                           void* bar, int gv0, int nv, int list_bytes) {
   constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
-  const int nl = list_bytes >> 4;
-  if (nv == 1 && NPP + N4 / 4 + nl < 32) {
-    // one 16-byte chunk per lane: z' rows | thresholds | lists; lane 31: (E_acc, corr)
-    const char* src;
-    float* dst;
-    if (lane < NPP) {
-      src = reinterpret_cast<const char*>(a.zq + (int64_t)gv0 * NPP + lane);
-      dst = buf + so.zs + 4 * lane;
-    } else if (lane < NPP + N4 / 4) {
-      src = reinterpret_cast<const char*>(a.thrg + (int64_t)gv0 * N4 + 4 * (lane - NPP));
-      dst = buf + so.thr + 4 * (lane - NPP);
-    } else {
-      src = reinterpret_cast<const char*>(a.lists + (int64_t)gv0 * list_bytes) +
-            16 * (lane - NPP - N4 / 4);
-      dst = buf + so.lst + 4 * (lane - NPP - N4 / 4);
-    }
-    if (lane < NPP + N4 / 4 + nl) cp_async16(dst, src);
-    if (lane == 31) cp_async8(buf + so.eac, a.vaux + gv0);
-    cp_async_commit();
-    return;
-  }
-  const float4* zsrc = a.zq + (int64_t)gv0 * NPP;
-  for (int i = lane; i < nv * NPP; i += 32) cp_async16(buf + so.zs + 4 * i, zsrc + i);
-  const float* tsrc = a.thrg + (int64_t)gv0 * N4;
-  for (int i = lane; i < nv * (N4 / 4); i += 32) cp_async16(buf + so.thr + 4 * i, tsrc + 4 * i);
-  if (lane < nv) cp_async8(buf + so.eac + 2 * lane, a.vaux + gv0 + lane);
-  if (list_bytes) {
-    const uint8_t* lsrc = a.lists + (int64_t)gv0 * list_bytes;
-    for (int i = lane; i < nv * (list_bytes >> 4); i += 32)
-      cp_async16(buf + so.lst + 4 * i, lsrc + 16 * i);
-  }
-  cp_async_commit();
+  const unsigned bz = nv * NPP * 16, bt = nv * N4 * 4, bl = nv * list_bytes;
+  const int e0 = gv0 & ~1;
+  const unsigned be = ((gv0 - e0 + nv) * 8 + 15) & ~15u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
+  mbar_expect_tx(bar, bz + bt + bl + be);
+  bulk_g2s(buf + so.zs, a.zq + (int64_t)gv0 * NPP, bz, bar);
+  bulk_g2s(buf + so.thr, a.thrg + (int64_t)gv0 * N4, bt, bar);
+  if (bl) bulk_g2s(buf + so.lst, a.lists + (int64_t)gv0 * list_bytes, bl, bar);
+  bulk_g2s(buf + so.eac, a.vaux + e0, be, bar);
 }
 
 // VPI = false: one vector per item, its P paths in bpv batches of 32 PT paths
@@ -916,6 +948,13 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   TreeParams& tp = *reinterpret_cast<TreeParams*>(sm + so.tpo);
   float* tab = sm + so.tab;
   float* wb0 = sm + so.wbuf + warp * 2 * so.bufsz;
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(sm + so.mbar) + 2 * warp;
+  if (lane == 0) {
+    mbar_init(wbar, 1);
+    mbar_init(wbar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned phase = 0u;   // parity bit per buffer
   int4* evb = reinterpret_cast<int4*>(sm + so.ev);
   int* evn = reinterpret_cast<int*>(sm + so.evn);
   {
@@ -946,7 +985,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
           const int d = p / tparam.stride[pos];
           if (e == L * L) {
             const int dd = d % e;
-            x = pk2((float)(dd / L), (float)(dd % L));
+            x = pk2(-(float)(dd / L), -(float)(dd % L));   // negated level indices
           } else {
             x = (u64)(unsigned)(tparam.list_off[pos] + d);
           }
@@ -973,28 +1012,39 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
     }
     __syncthreads();
+    // warp w owns the balanced item range [wb, we) of the segment, walked in
+    // chunks of so.ck items (contiguous vectors, one bulk-copy group each)
+    const int wb = seg + (int)((int64_t)warp * (seg_end - seg) / nw);
+    const int we = seg + (int)((int64_t)(warp + 1) * (seg_end - seg) / nw);
+    const int nchunk = (we - wb + so.ck - 1) / so.ck;
     int k = 0;
-    int it = seg + warp;
-    if (it < seg_end) {
-      const int j = (it - ibase) * nvi;
-      trav_prefetch<N>(a, so, wb0, vbase + j, min(nvi, V - j), lbytes, lane);
+    int ch = 0;
+    if (ch < nchunk && lane == 0) {
+      const int i0 = wb;
+      const int i1 = min(we, i0 + so.ck);
+      trav_issue<N>(a, so, wb0, wbar, vbase + (i0 - ibase) * nvi,
+                    min((i1 - ibase) * nvi, V) - (i0 - ibase) * nvi, lbytes);
     }
-    for (; it < seg_end; it += nw, k ^= 1) {
-      const int nxt = it + nw;
-      if (nxt < seg_end) {
-        const int j = (nxt - ibase) * nvi;
-        trav_prefetch<N>(a, so, wb0 + (k ^ 1) * so.bufsz, vbase + j, min(nvi, V - j), lbytes,
-                         lane);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
+    for (; ch < nchunk; ++ch, k ^= 1) {
+      if (ch + 1 < nchunk && lane == 0) {
+        const int i0 = wb + (ch + 1) * so.ck;
+        const int i1 = min(we, i0 + so.ck);
+        trav_issue<N>(a, so, wb0 + (k ^ 1) * so.bufsz, wbar + (k ^ 1),
+                      vbase + (i0 - ibase) * nvi, min((i1 - ibase) * nvi, V) - (i0 - ibase) * nvi,
+                      lbytes);
       }
-      __syncwarp();
-      const float* buf = wb0 + k * so.bufsz;
-      const float4* zs = reinterpret_cast<const float4*>(buf + so.zs);
-      const float* thr = buf + so.thr;
-      const float* weacc = buf + so.eac;                    // (E_acc, corr) pairs
-      const uint8_t* lch = reinterpret_cast<const uint8_t*>(buf + so.lst);
+      mbar_wait(wbar + k, (phase >> k) & 1u);
+      phase ^= 1u << k;
+      const float* cbuf = wb0 + k * so.bufsz;
+      const int ci0 = wb + ch * so.ck;
+      const int ci1 = min(we, ci0 + so.ck);
+      const int eo = (vbase + (ci0 - ibase) * nvi) & 1;   // (E_acc, corr) window offset
+    for (int it = ci0; it < ci1; ++it) {
+      const int jl = (it - ci0) * nvi;                      // vector offset in the chunk
+      const float4* zs = reinterpret_cast<const float4*>(cbuf + so.zs) + jl * ((N + 1) / 2);
+      const float* thr = cbuf + so.thr + jl * ((N + 3) & ~3);
+      const float* weacc = cbuf + so.eac + 2 * (eo + jl);   // (E_acc, corr) pairs
+      const uint8_t* lch = reinterpret_cast<const uint8_t*>(cbuf + so.lst) + jl * lbytes;
       const int jv = (it - ibase) * nvi;
       const int gbase = vbase + jv;
       const int vce = min(nvi, V - jv);
@@ -1009,8 +1059,8 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         const float4 zt = zs[(N - 1) >> 1];
         const float ur = ((N - 1) & 1) ? zt.z : zt.x, ui = ((N - 1) & 1) ? zt.w : zt.y;
         float t0;
-        const float kxt = T.lay4[N - 1].x;
-        const int d0 = (int)slice_axis<L>(ur, kxt, t0) * L + (int)slice_axis<L>(ui, kxt, t0);
+        const float kxt = T.lay4[N - 1].w;
+        const int d0 = (int)(-slice_axis<L>(ur, kxt, t0)) * L + (int)(-slice_axis<L>(ui, kxt, t0));
         b0 = (d0 * tp.stride[N - 1]) / S;
       }
       for (int bi = 0; bi < bpv; ++bi) {
@@ -1112,7 +1162,8 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
           a.vpath[gbase] = make_int2((int)q1, (int)q2);
         }
       }
-      __syncwarp();   // the buffer is refilled by the prefetch two items ahead
+    }
+      __syncwarp();   // the chunk buffer is refilled by the next issue into it
     }
     seg = seg_end;
   }
@@ -1245,8 +1296,8 @@ __device__ __forceinline__ void warp_retrace(const float* tab, int m, const floa
       fi = (float)ii;
     } else {
       float tr, ti;
-      const float sr = slice_axis<L>(ar, ly.x, tr);
-      const float si = slice_axis<L>(ai, ly.x, ti);
+      const float sr = -slice_axis<L>(ar, ly.w, tr);   // level indices (positive form)
+      const float si = -slice_axis<L>(ai, ly.w, ti);
       fr = __shfl_sync(0xffffffffu, sr, pos);
       fi = __shfl_sync(0xffffffffu, si, pos);
     }
