@@ -1269,15 +1269,15 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
 // The fp32 re-trace is warp-cooperative (lane = tree row) with exactly the
 // traversal's per-row fma sequence, so it reproduces the traversal bit for bit.
 // ===========================================================================
-// fp32 re-trace of path p with lanes = rows; labw[pos] / prew[pos] (smem) for pos >= stop
+// fp32 re-trace of path p with lanes = rows; labw[pos] / prew[pos] (smem) for pos >= stop.
+// T / zrow may point to global or (staged) shared memory.
 template <int N, int L>
-__device__ __forceinline__ void warp_retrace(const float* tab, int m, const float4* zrow,
+__device__ __forceinline__ void warp_retrace(const TabPtrs& T, const float4* zrow,
                                              const uint8_t* vlist, const TreeParams& tp, int p,
                                              int stop, int* labw, float* prew) {
   constexpr int NPP = (N + 1) / 2;
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
   const int lane = threadIdx.x & 31;
-  const TabPtrs T = tab_ptrs(tab, m, N);
   float ar = 0.f, ai = 0.f;
   if (lane < N) {
     const float2 zf = reinterpret_cast<const float2*>(zrow)[lane];
@@ -1286,8 +1286,11 @@ __device__ __forceinline__ void warp_retrace(const float* tab, int m, const floa
   }
   u64 ped2 = 0ull;
   const int top_lo = N - tp.n_top;
-  for (int pos = N - 1; pos >= stop; --pos) {
+#pragma unroll
+  for (int pos = N - 1; pos >= 0; --pos) {
+    if (pos < stop) break;
     const float4 ly = T.lay4[pos];
+    const float2 rr = (lane < pos) ? rcol_at(T.rcol, NPP, lane, pos) : make_float2(0.f, 0.f);
     float fr, fi;
     if (pos >= N - XM && pos >= top_lo) {
       int ir, ii;
@@ -1312,7 +1315,6 @@ __device__ __forceinline__ void warp_retrace(const float* tab, int m, const floa
     const u64 e2 = pk2(er, ei);
     ped2 = ffma2(e2, e2, ped2);
     if (lane < pos) {
-      const float2 rr = rcol_at(T.rcol, NPP, lane, pos);
       ar = __fmaf_rn(rr.x, fr, ar);
       ar = __fmaf_rn(rr.y, -fi, ar);
       ai = __fmaf_rn(rr.x, fi, ai);
@@ -1322,70 +1324,73 @@ __device__ __forceinline__ void warp_retrace(const float* tab, int m, const floa
   __syncwarp();
 }
 
-// fp64 centre of layer pos for the path whose level indices above pos are labw (smem)
-__device__ __forceinline__ void warp_centre_f64(const DetectArgs& a, const float* tab, int64_t c,
-                                                int64_t gv, int n, int L, int pos,
-                                                const int* labw, double& cr, double& ci) {
+// fp64 rotation z_k = (Q^H y)_k for lane k < n (sequential over the receive
+// rows; the channel's transposed Q^H from its table blob, coalesced over k;
+// y_r broadcast by shuffles from the lane that loaded it).
+__device__ __forceinline__ void warp_z_f64(const DetectArgs& a, const float* tab, int64_t gv,
+                                           int n, double& zr, double& zi) {
   const int lane = threadIdx.x & 31;
   const int m = a.m;
-  const TableLayout tl(m, n);
-  const double2* qt = reinterpret_cast<const double2*>(tab + tl.off_qh);
-  const double nrm = qam_norm_d(L);
-  double zr = 0.0, zi = 0.0;
-  for (int r = lane; r < m; r += 32) {
-    double yr, yi;
-    if (a.y_f64) {
-      const double2 v = reinterpret_cast<const double2*>(a.y)[gv * m + r];
-      yr = v.x; yi = v.y;
-    } else {
-      const float2 v = reinterpret_cast<const float2*>(a.y)[gv * m + r];
-      yr = v.x; yi = v.y;
-    }
-    const double2 q = a.qh64[(c * n + pos) * (int64_t)m + r];
+  const double2* qt = reinterpret_cast<const double2*>(tab + TableLayout(m, n).off_qh);
+  double y0r = 0.0, y0i = 0.0, y1r = 0.0, y1i = 0.0;   // y_lane, y_{lane+32}
+  if (a.y_f64) {
+    const double2* yp = reinterpret_cast<const double2*>(a.y) + gv * m;
+    if (lane < m) { const double2 v = yp[lane]; y0r = v.x; y0i = v.y; }
+    if (lane + 32 < m) { const double2 v = yp[lane + 32]; y1r = v.x; y1i = v.y; }
+  } else {
+    const float2* yp = reinterpret_cast<const float2*>(a.y) + gv * m;
+    if (lane < m) { const float2 v = yp[lane]; y0r = v.x; y0i = v.y; }
+    if (lane + 32 < m) { const float2 v = yp[lane + 32]; y1r = v.x; y1i = v.y; }
+  }
+  const int k = lane < n ? lane : n - 1;
+  zr = 0.0;
+  zi = 0.0;
+#pragma unroll 8
+  for (int r = 0; r < m; ++r) {
+    const double2 q = qt[r * n + k];
+    const double yr = __shfl_sync(0xffffffffu, r < 32 ? y0r : y1r, r & 31);
+    const double yi = __shfl_sync(0xffffffffu, r < 32 ? y0i : y1i, r & 31);
     zr = fma(q.x, yr, fma(-q.y, yi, zr));
     zi = fma(q.x, yi, fma(q.y, yr, zi));
   }
+}
+
+// fp64 centre of layer pos for the path whose level indices above pos are labw
+// (smem); zr/zi = this lane's fp64 rotation (warp_z_f64)
+__device__ __forceinline__ void warp_centre_f64(const DetectArgs& a, int64_t c, int n, int L,
+                                                int pos, const int* labw, double zr, double zi,
+                                                double& cr, double& ci) {
+  const int lane = threadIdx.x & 31;
+  const double nrm = qam_norm_d(L);
+  const double* R = reinterpret_cast<const double*>(a.r64 + (c * n + pos) * (int64_t)n);
+  double sr_ = 0.0, si_ = 0.0;
   const int j = pos + 1 + lane;
   if (j < n) {
     const double sr = level_value(labw[j] >> 3, L, nrm), si = level_value(labw[j] & 7, L, nrm);
-    const double2 r = a.r64[(c * n + pos) * (int64_t)n + j];
-    zr -= r.x * sr - r.y * si;
-    zi -= r.x * si + r.y * sr;
+    const double rr = R[2 * j], ri = R[2 * j + 1];
+    sr_ = rr * sr - ri * si;
+    si_ = rr * si + ri * sr;
   }
-  (void)qt;
-  zr = warp_sum_d(zr);
-  zi = warp_sum_d(zi);
-  const double rpp = a.r64[(c * n + pos) * (int64_t)n + pos].x;
-  cr = zr / rpp;
-  ci = zi / rpp;
+  sr_ = warp_sum_d(sr_);
+  si_ = warp_sum_d(si_);
+  const double zp_r = __shfl_sync(0xffffffffu, zr, pos), zp_i = __shfl_sync(0xffffffffu, zi, pos);
+  const double rpp = R[2 * pos];
+  cr = (zp_r - sr_) / rpp;
+  ci = (zp_i - si_) / rpp;
 }
 
 // fp64 PED ||z - R x||^2 of the path with level indices labw (smem), lanes = rows
-__device__ __forceinline__ double warp_ped_f64(const DetectArgs& a, int64_t c, int64_t gv, int n,
-                                               int L, const int* labw) {
+__device__ __forceinline__ double warp_ped_f64(const DetectArgs& a, int64_t c, int n, int L,
+                                               const int* labw, double zr, double zi) {
   const int lane = threadIdx.x & 31;
-  const int m = a.m;
   const double nrm = qam_norm_d(L);
   double acc = 0.0;
   if (lane < n) {
-    const int k = lane;
-    double zr = 0.0, zi = 0.0;
-    for (int r = 0; r < m; ++r) {
-      double yr, yi;
-      if (a.y_f64) {
-        const double2 v = reinterpret_cast<const double2*>(a.y)[gv * m + r];
-        yr = v.x; yi = v.y;
-      } else {
-        const float2 v = reinterpret_cast<const float2*>(a.y)[gv * m + r];
-        yr = v.x; yi = v.y;
-      }
-      const double2 q = a.qh64[(c * n + k) * (int64_t)m + r];
-      zr = fma(q.x, yr, fma(-q.y, yi, zr));
-      zi = fma(q.x, yi, fma(q.y, yr, zi));
-    }
-    for (int j = k; j < n; ++j) {
+    const double2* R = a.r64 + (c * n + lane) * (int64_t)n;
+#pragma unroll 4
+    for (int j = lane; j < n; ++j) {
       const double sr = level_value(labw[j] >> 3, L, nrm), si = level_value(labw[j] & 7, L, nrm);
-      const double2 r = a.r64[(c * n + k) * (int64_t)n + j];
+      const double2 r = R[j];
       zr -= r.x * sr - r.y * si;
       zi -= r.x * si + r.y * sr;
     }
@@ -1396,38 +1401,27 @@ __device__ __forceinline__ double warp_ped_f64(const DetectArgs& a, int64_t c, i
 
 // The reference's path from layer pos down, in fp64: prefix symbols labw[j > pos],
 // the fp64 decision (ir0, ii0) at pos, exact SIC below.  Returns its fp64 PED.
-// Lanes = rows.
-__device__ __forceinline__ double warp_sic_f64(const DetectArgs& a, int64_t c, int64_t gv, int n,
-                                               int L, int pos, const int* labw, int ir0,
-                                               int ii0) {
+// Lanes = rows; zr/zi = this lane's fp64 rotation.
+__device__ __forceinline__ double warp_sic_f64(const DetectArgs& a, int64_t c, int n, int L,
+                                               int pos, const int* labw, int ir0, int ii0,
+                                               double zr, double zi) {
   const int lane = threadIdx.x & 31;
-  const int m = a.m;
   const double nrm = qam_norm_d(L);
   const double2* R = a.r64 + c * (int64_t)n * n;
-  double zr = 0.0, zi = 0.0;
   if (lane < n) {
-    for (int r = 0; r < m; ++r) {
-      double yr, yi;
-      if (a.y_f64) {
-        const double2 v = reinterpret_cast<const double2*>(a.y)[gv * m + r];
-        yr = v.x; yi = v.y;
-      } else {
-        const float2 v = reinterpret_cast<const float2*>(a.y)[gv * m + r];
-        yr = v.x; yi = v.y;
-      }
-      const double2 q = a.qh64[(c * n + lane) * (int64_t)m + r];
-      zr = fma(q.x, yr, fma(-q.y, yi, zr));
-      zi = fma(q.x, yi, fma(q.y, yr, zi));
-    }
     // interference of the prefix symbols (j > pos); rows above pos also add
     // their own symbol and become prefix residuals
     const int j0 = lane > pos ? lane : pos + 1;
+#pragma unroll 4
     for (int j = j0; j < n; ++j) {
       const double sr = level_value(labw[j] >> 3, L, nrm), si = level_value(labw[j] & 7, L, nrm);
       const double2 r = R[lane * n + j];
       zr -= r.x * sr - r.y * si;
       zi -= r.x * si + r.y * sr;
     }
+  } else {
+    zr = 0.0;
+    zi = 0.0;
   }
   double ped = (lane > pos && lane < n) ? zr * zr + zi * zi : 0.0;
   for (int q = pos; q >= 0; --q) {
@@ -1449,101 +1443,155 @@ __device__ __forceinline__ double warp_sic_f64(const DetectArgs& a, int64_t c, i
   return warp_sum_d(ped);
 }
 
+// K4b event checks: one warp per event, events strided over all warps.  Each
+// warp double-buffers its events' traversal tables (lay + r'' columns, one
+// contiguous block of the channel's blob) and z' rows in shared memory with
+// cp.async, so the next event's fetch overlaps this event's re-trace.
+#define CHECK_WARPS 4
+template <int N>
+struct CheckSmem {
+  static constexpr int NPP = (N + 1) / 2;
+  static constexpr int TW = N + N * NPP;   // float4: lay | rcol
+  float4 tab[CHECK_WARPS][2][TW];
+  float4 z[CHECK_WARPS][2][NPP];
+  int labs[CHECK_WARPS][2][MPNL_MAX_N];
+  float pres[CHECK_WARPS][MPNL_MAX_N];
+  TreeParams tp;
+};
+
+template <int N>
+__device__ __forceinline__ void check_fetch(const DetectArgs& a, const TableLayout& tl, int4 e4,
+                                            float4* tb, float4* zb, int lane) {
+  constexpr int NPP = (N + 1) / 2, TW = N + N * NPP;
+  const int64_t gv = (int64_t)(unsigned)e4.z;
+  const int64_t c = gv / a.V;
+  const float4* src = reinterpret_cast<const float4*>(a.tables + c * (int64_t)tl.total + tl.off_lay);
+  for (int i = lane; i < TW; i += 32) cp_async16(tb + i, src + i);
+  if (lane < NPP) cp_async16(zb + lane, a.zq + gv * NPP + lane);
+  cp_async_commit();
+}
+
 template <int N, int L>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(32 * CHECK_WARPS)
 check_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
   (void)unused;
-  __shared__ TreeParams tp;
-  __shared__ int labs[4][2][MPNL_MAX_N];
-  __shared__ float pres[4][MPNL_MAX_N];
+  extern __shared__ __align__(16) uint8_t csm_raw[];
+  CheckSmem<N>& S = *reinterpret_cast<CheckSmem<N>*>(csm_raw);
+  TreeParams& tp = S.tp;
   {
     const int* s = reinterpret_cast<const int*>(&tparam);
     int* d = reinterpret_cast<int*>(&tp);
     for (int i = threadIdx.x; i < (int)(sizeof(TreeParams) / 4); i += blockDim.x) d[i] = s[i];
   }
   __syncthreads();
-  constexpr int NPP = (N + 1) / 2;
   const int m = a.m;
   const TableLayout tl(m, N);
   const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
   const double nrm = qam_norm_d(L);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int* lab = labs[warp][0];
-  int* lab2 = labs[warp][1];
-  float* pre = pres[warp];
+  int* lab = S.labs[warp][0];
+  int* lab2 = S.labs[warp][1];
+  float* pre = S.pres[warp];
   const int nev = min(a.counters[1], a.ev_cap);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
-  for (int i = blockIdx.x * (blockDim.x >> 5) + warp; i < nev; i += nwarps) {
-    const int4 e4 = a.events[i];
-    const int64_t gv = (int64_t)(unsigned)e4.z;
-    if (a.vflag[gv]) continue;
-    const int64_t c = gv / a.V;
-    const float* tab = a.tables + c * (int64_t)tl.total;
-    const float4* zrow = a.zq + gv * NPP;
-    const uint8_t* vlist = a.lists + gv * tp.list_bytes;
-    const float4 res = a.vres[gv];
-    const float lim = res.x + 2.f * ped_tol(res.x, res.w, N);
-    if (e4.w == EV_NODE) {
-      const unsigned mask = (unsigned)e4.y;
-      const int lowest = __ffs(mask) - 1;
-      warp_retrace<N, L>(tab, m, zrow, vlist, tp, e4.x, lowest, lab, pre);
-      for (int pos = N - 1; pos >= lowest; --pos) {
-        if (!((mask >> pos) & 1u) || pre[pos] > lim) continue;
-        if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
-        double cr, ci;
-        warp_centre_f64(a, tab, c, gv, N, L, pos, lab, cr, ci);
-        const int ir = nearest_level_f64(cr, L, nrm), ii = nearest_level_f64(ci, L, nrm);
-        if (ir * 8 + ii != lab[pos]) {
-          // the reference takes the other branch here.  Our fp32 path is then
-          // a candidate the reference lacks: harmless unless it is one of our
-          // two best.  The reference's path instead: harmless unless its exact
-          // metric could beat our winner.
-          const int2 pth = a.vpath[gv];
-          bool bad = e4.x == pth.x || e4.x == pth.y;
-          if (!bad) {
-            const double malt = warp_sic_f64(a, c, gv, N, L, pos, lab, ir, ii);
-            bad = malt <= (double)lim;
-          }
-          if (bad && lane == 0) send_to_fp64(a, gv, 2);
-          break;
-        }
-      }
-    } else if (e4.w == EV_CUT) {
-      const int pos = e4.y;
-      if (pos < N - 1) warp_retrace<N, L>(tab, m, zrow, vlist, tp, e4.x, pos + 1, lab, pre);
-      const float prefix = (pos < N - 1) ? pre[pos + 1] : 0.f;   // <= PED prefix at pos
-      if (prefix > lim) continue;
-      if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
-      double cr, ci;
-      warp_centre_f64(a, tab, c, gv, N, L, pos, lab, cr, ci);
-      if (lane == 0) {
-        const int e = tp.e[pos];
-        const unsigned long long m64 = nearest_set_f64(cr, ci, L, nrm, e);
-        const int par = e4.x / tp.stride[pos + 1];
-        const uint8_t* lst = vlist + tp.list_off[pos] + par * e;
-        unsigned long long m32 = 0ull;
-        for (int r = 0; r < e; ++r) m32 |= 1ull << ((lst[r] >> 3) * L + (lst[r] & 7));
-        if (m32 != m64) send_to_fp64(a, gv, 2);
-      }
-    } else {   // EV_TIE: fp64 metrics of the two best paths
-      if (a.stats && lane == 0) atomicAdd(a.stats + 2, 1);
-      warp_retrace<N, L>(tab, m, zrow, vlist, tp, e4.x, 0, lab, pre);
-      warp_retrace<N, L>(tab, m, zrow, vlist, tp, e4.y, 0, lab2, pre);
-      const double m1 = warp_ped_f64(a, c, gv, N, L, lab);
-      const double m2 = warp_ped_f64(a, c, gv, N, L, lab2);
-      if (fabs(m1 - m2) <= 1e-12 * fmax(m1, m2)) {
-        if (lane == 0) send_to_fp64(a, gv, 1);   // tie at fp64 level: exact total order
-      } else if (m2 < m1) {
-        // the second path wins: rewrite labels and metric (fp32 value of that path)
-        const int32_t* pc = a.perm + c * N;
-        if (lane < N) {
-          const int ir = lab2[lane] >> 3, ii = lab2[lane] & 7;
-          a.hard[gv * N + pc[lane]] = (uint8_t)((gray_code(ir) << h) | gray_code(ii));
-        }
-        if (lane == 0) a.metric[gv] = a.metric[gv] - res.x + res.y;
-      }
+  int i = blockIdx.x * (blockDim.x >> 5) + warp;
+  int k = 0;
+  int4 e4 = make_int4(0, 0, 0, 0);
+  if (i < nev) {
+    e4 = a.events[i];
+    check_fetch<N>(a, tl, e4, S.tab[warp][0], S.z[warp][0], lane);
+  }
+  for (; i < nev; i += nwarps, k ^= 1) {
+    int4 en = make_int4(0, 0, 0, 0);
+    if (i + nwarps < nev) {
+      en = a.events[i + nwarps];
+      check_fetch<N>(a, tl, en, S.tab[warp][k ^ 1], S.z[warp][k ^ 1], lane);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncwarp();
+    const int64_t gv = (int64_t)(unsigned)e4.z;
+    if (!a.vflag[gv]) {
+      const int64_t c = gv / a.V;
+      const float* tab = a.tables + c * (int64_t)tl.total;
+      TabPtrs T;
+      T.lay4 = S.tab[warp][k];
+      T.rcol = reinterpret_cast<const float*>(S.tab[warp][k] + N);
+      const float4* zrow = S.z[warp][k];
+      const uint8_t* vlist = a.lists + gv * tp.list_bytes;
+      const float4 res = a.vres[gv];
+      const float lim = res.x + 2.f * ped_tol(res.x, res.w, N);
+      if (e4.w == EV_NODE) {
+        const unsigned mask = (unsigned)e4.y;
+        const int lowest = __ffs(mask) - 1;
+        warp_retrace<N, L>(T, zrow, vlist, tp, e4.x, lowest, lab, pre);
+        bool zdone = false;
+        double zr = 0.0, zi = 0.0;
+        for (int pos = N - 1; pos >= lowest; --pos) {
+          if (!((mask >> pos) & 1u) || pre[pos] > lim) continue;
+          if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
+          if (!zdone) { warp_z_f64(a, tab, gv, N, zr, zi); zdone = true; }
+          double cr, ci;
+          warp_centre_f64(a, c, N, L, pos, lab, zr, zi, cr, ci);
+          const int ir = nearest_level_f64(cr, L, nrm), ii = nearest_level_f64(ci, L, nrm);
+          if (ir * 8 + ii != lab[pos]) {
+            // the reference takes the other branch here.  Our fp32 path is then
+            // a candidate the reference lacks: harmless unless it is one of our
+            // two best.  The reference's path instead: harmless unless its exact
+            // metric could beat our winner.
+            const int2 pth = a.vpath[gv];
+            bool bad = e4.x == pth.x || e4.x == pth.y;
+            if (!bad) {
+              const double malt = warp_sic_f64(a, c, N, L, pos, lab, ir, ii, zr, zi);
+              bad = malt <= (double)lim;
+            }
+            if (bad && lane == 0) send_to_fp64(a, gv, 2);
+            break;
+          }
+        }
+      } else if (e4.w == EV_CUT) {
+        const int pos = e4.y;
+        if (pos < N - 1) warp_retrace<N, L>(T, zrow, vlist, tp, e4.x, pos + 1, lab, pre);
+        const float prefix = (pos < N - 1) ? pre[pos + 1] : 0.f;   // <= PED prefix at pos
+        if (prefix <= lim) {
+          if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
+          double zr, zi, cr, ci;
+          warp_z_f64(a, tab, gv, N, zr, zi);
+          warp_centre_f64(a, c, N, L, pos, lab, zr, zi, cr, ci);
+          if (lane == 0) {
+            const int e = tp.e[pos];
+            const unsigned long long m64 = nearest_set_f64(cr, ci, L, nrm, e);
+            const int par = e4.x / tp.stride[pos + 1];
+            const uint8_t* lst = vlist + tp.list_off[pos] + par * e;
+            unsigned long long m32 = 0ull;
+            for (int r = 0; r < e; ++r) m32 |= 1ull << ((lst[r] >> 3) * L + (lst[r] & 7));
+            if (m32 != m64) send_to_fp64(a, gv, 2);
+          }
+        }
+      } else {   // EV_TIE: fp64 metrics of the two best paths
+        if (a.stats && lane == 0) atomicAdd(a.stats + 2, 1);
+        warp_retrace<N, L>(T, zrow, vlist, tp, e4.x, 0, lab, pre);
+        warp_retrace<N, L>(T, zrow, vlist, tp, e4.y, 0, lab2, pre);
+        double zr, zi;
+        warp_z_f64(a, tab, gv, N, zr, zi);
+        const double m1 = warp_ped_f64(a, c, N, L, lab, zr, zi);
+        const double m2 = warp_ped_f64(a, c, N, L, lab2, zr, zi);
+        if (fabs(m1 - m2) <= 1e-12 * fmax(m1, m2)) {
+          if (lane == 0) send_to_fp64(a, gv, 1);   // tie at fp64 level: exact total order
+        } else if (m2 < m1) {
+          // the second path wins: rewrite labels and metric (fp32 value of that path)
+          const int32_t* pc = a.perm + c * N;
+          if (lane < N) {
+            const int ir = lab2[lane] >> 3, ii = lab2[lane] & 7;
+            a.hard[gv * N + pc[lane]] = (uint8_t)((gray_code(ir) << h) | gray_code(ii));
+          }
+          if (lane == 0) a.metric[gv] = a.metric[gv] - res.x + res.y;
+        }
+      }
+    }
+    __syncwarp();   // this buffer is refilled by the fetch two events ahead
+    e4 = en;
   }
 }
 

@@ -51,7 +51,16 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
   } else if (kind == 2) {
     verify_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
   } else {
-    check_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
+    // events strided over all warps; at most the resident capacity
+    auto k = check_kernel<NN, L>;
+    const int sm = (int)sizeof(CheckSmem<NN>);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    int nb = 0, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 32 * CHECK_WARPS, sm);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = (unsigned)std::min<long long>((long long)std::max(nb, 1) * sms, (long long)grid);
+    k<<<grid, 32 * CHECK_WARPS, sm, st>>>(a, tp, extra);
   }
   return cudaGetLastError();
 }
