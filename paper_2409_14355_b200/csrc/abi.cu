@@ -313,24 +313,27 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     if (e == cudaSuccess) e = cudaMemsetAsync(a.vflag, 0, 4 * B, st);
     if (e != cudaSuccess) return cuda_fail(e, "memset");
     if (slow) return MPNL_OK;
-    // per-vector preparation (z', guard thresholds): CTA = vg x 32 vectors of a
-    // channel; the largest vg whose last chunk wastes <= 5% (and fits smem / 1024 threads)
-    {
-      int vg = 1;
-      for (int g = 4; g >= 2; g >>= 1) {
-        const int64_t vc = 32 * g, ch = (v_per_ch + vc - 1) / vc;
-        if (PrepSmem::threads(n, g) <= 1024 && PrepSmem(m, n, g).total <= 200 * 1024 &&
-            (double)v_per_ch >= 0.95 * (double)(ch * vc)) { vg = g; break; }
-      }
-      const int64_t vc = 32 * vg, pch = (v_per_ch + vc - 1) / vc;
-      if (n_ch * pch > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
-      const PrepSmem ps(m, n, vg);
-      e = launch_fast(n, L, 4, a, tp, (unsigned)(n_ch * pch), PrepSmem::threads(n, vg), ps.total,
-                      (int)pch, st);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "prep kernel");
+    // partial (1 < e < Q) layers among the expanded ones; the top one is
+    // selected inside the fused prep kernel when it is the top layer or sits
+    // right below a full top layer, any other by the generic select kernel
+    int fused = -1;
     for (int pos = n - 1; pos >= n - tp.n_top; --pos) {
       if (tp.e[pos] == L * L) continue;
+      if (tp.e[pos] <= 4 && (pos == n - 1 || (pos == n - 2 && tp.e[n - 1] == L * L)))
+        fused = pos;
+      break;
+    }
+    // one thread per vector for large batches; 4 (rows and parents split) when
+    // a thread per vector would leave the SMs short of warps
+    const int tpv = B >= 148 * 128 * 8 ? 1 : 4;
+    const int64_t pch = (v_per_ch + 128 / tpv - 1) / (128 / tpv);
+    if (n_ch * pch > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
+    if (16 * (m + 2) * n + 128 * 16 * (m | 1) > 200 * 1024)
+      return fail(MPNL_EUNSUPPORTED, "channel too large");
+    e = launch_fast(n, L, 5, a, tp, 0, tpv, 0, fused, st);
+    if (e != cudaSuccess) return cuda_fail(e, "prep kernel");
+    for (int pos = n - 1; pos >= n - tp.n_top; --pos) {
+      if (tp.e[pos] == L * L || pos == fused) continue;
       const int npar = tp.n_paths / tp.stride[pos + 1];
       const int px = std::min(npar, 128), vy = std::max(1, 128 / px);
       if (n_ch * ((v_per_ch + vy - 1) / vy) > 0x7fffffffLL || (npar + px - 1) / px > 65535)

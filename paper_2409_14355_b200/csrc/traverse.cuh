@@ -512,149 +512,6 @@ __device__ __forceinline__ void group_top3(Top3 t, int width, float& b1, unsigne
 }
 
 // ===========================================================================
-// K1b: per-vector preparation.  CTA = a channel's chunk of vg x 32 vectors,
-// warp = (32-vector group, block of 4 rows), lane = vector: the channel's fp64
-// Q^H (transposed) is read as warp-uniform broadcasts, each lane's y_r feeds 4
-// rows.  z'_k = fl32((Q^H y)_k - shift_k) (fp64 rotation, one rounding), the
-// per-layer guard thresholds of the fp32 traversal, then per vector E_acc (L2
-// over layers) and the M > N metric offset (fixed-order sums).  Results are
-// staged in shared memory and written as contiguous rows.
-// ===========================================================================
-#define PREP_RB 4   // rows per warp
-
-// vg = 32-vector groups per CTA (CTA = vg * 32 vectors of one channel)
-struct PrepSmem {
-  int vc, qt, sh, ly, y, z, th, e2, zn, total;   // bytes
-  __host__ __device__ PrepSmem(int m, int n, int vg) {
-    const int npp = (n + 1) / 2, n4 = (n + 3) & ~3;
-    vc = 32 * vg;
-    int o = 0;
-    qt = o; o += 16 * m * n;
-    sh = o; o += 16 * n;
-    ly = o; o += 16 * n;
-    y = o; o += 16 * vc * (m + 1);        // padded rows (bank spread)
-    z = o; o += 8 * vc * (2 * npp + 1);   // staged z' rows (float2, padded stride)
-    th = o; o += 4 * vc * (n4 + 1);       // staged thresholds (padded stride)
-    e2 = o; o += 8 * vc * 9;              // per (row block, vector) partial sums; [8]: ||y||^2
-    zn = o; o += 8 * vc * 8;
-    total = o;
-  }
-  __host__ __device__ static int nrb(int n) { return (n + PREP_RB - 1) / PREP_RB; }
-  __host__ __device__ static int threads(int n, int vg) { return 32 * vg * nrb(n); }
-};
-
-template <int N, int L>
-__global__ void __launch_bounds__(1024)
-prep_kernel(const DetectArgs a, const TreeParams tparam, int chunks) {
-  (void)tparam;
-  constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
-  constexpr int NRB = (N + PREP_RB - 1) / PREP_RB;
-  extern __shared__ __align__(16) uint8_t psm[];
-  const int m = a.m;
-  const int vg = blockDim.x / (32 * NRB);
-  const PrepSmem so(m, N, vg);
-  const int VC = so.vc;
-  double2* qt = reinterpret_cast<double2*>(psm + so.qt);
-  double2* sh = reinterpret_cast<double2*>(psm + so.sh);
-  float4* ly = reinterpret_cast<float4*>(psm + so.ly);
-  double2* ys = reinterpret_cast<double2*>(psm + so.y);
-  float2* zst = reinterpret_cast<float2*>(psm + so.z);
-  float* tst = reinterpret_cast<float*>(psm + so.th);
-  double* e2s = reinterpret_cast<double*>(psm + so.e2);
-  double* zns = reinterpret_cast<double*>(psm + so.zn);
-  const TableLayout tl(m, N);
-  const int64_t c = blockIdx.x / chunks;
-  const int v0 = (blockIdx.x % chunks) * VC;
-  const int vce = (int)min((int64_t)VC, a.V - v0);
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const float* tab = a.tables + c * (int64_t)tl.total;
-  const int64_t g0 = c * a.V + v0;
-  {
-    const double2* q = reinterpret_cast<const double2*>(tab + tl.off_qh);
-    for (int i = tid; i < m * N; i += nth) qt[i] = q[i];
-    const double2* s2 = reinterpret_cast<const double2*>(tab + tl.off_shift);
-    const float4* l4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
-    for (int i = tid; i < N; i += nth) { sh[i] = s2[i]; ly[i] = l4[i]; }
-    // flat copy; (v, r) by a float reciprocal (exact for i < 2^13: v*m + r <= 128*64)
-    const float rm = 1.f / (float)m;
-    for (int i = tid; i < vce * m; i += nth) {
-      const int v = (int)(((float)i + 0.5f) * rm), r = i - v * m;
-      double2 yv;
-      if (a.y_f64) {
-        yv = reinterpret_cast<const double2*>(a.y)[g0 * m + i];
-      } else {
-        const float2 f = reinterpret_cast<const float2*>(a.y)[g0 * m + i];
-        yv = make_double2(f.x, f.y);
-      }
-      ys[v * (m + 1) + r] = yv;
-    }
-  }
-  __syncthreads();
-  // warp = (vector group, row block); lane = vector
-  const int rb = warp % NRB;
-  const int v = (warp / NRB) * 32 + lane;
-  const int k0 = rb * PREP_RB;
-  if (v < vce) {
-    const double2* yv = ys + v * (m + 1);
-    double zr[PREP_RB], zi[PREP_RB];
-#pragma unroll
-    for (int j = 0; j < PREP_RB; ++j) { zr[j] = 0.0; zi[j] = 0.0; }
-    double yn = 0.0;
-    for (int r = 0; r < m; ++r) {
-      const double2 y = yv[r];
-      yn = fma(y.x, y.x, fma(y.y, y.y, yn));
-#pragma unroll
-      for (int j = 0; j < PREP_RB; ++j) {
-        if (k0 + j < N) {
-          const double2 q = qt[r * N + k0 + j];   // warp-uniform broadcast
-          zr[j] = fma(q.x, y.x, zr[j]);
-          zr[j] = fma(-q.y, y.y, zr[j]);
-          zi[j] = fma(q.x, y.y, zi[j]);
-          zi[j] = fma(q.y, y.x, zi[j]);
-        }
-      }
-    }
-    const float ynf = (float)sqrt(yn) * 1.0001f;
-    double e2p = 0.0, znp = 0.0;
-#pragma unroll
-    for (int j = 0; j < PREP_RB; ++j) {
-      const int k = k0 + j;
-      if (k < N) {
-        const float2 z = make_float2((float)(zr[j] - sh[k].x), (float)(zi[j] - sh[k].y));
-        zst[v * (2 * NPP + 1) + k] = z;   // (re, im) per row
-        const float4 lk = ly[k];
-        const float e = row_bound(ynf, z, lk, k, m, N, L, a.guard_scale, 0);
-        tst[v * (N4 + 1) + k] = 0.5f - e / lk.y - MPNL_U * 3.f * L;
-        e2p += (double)e * e;
-        znp += zr[j] * zr[j] + zi[j] * zi[j];
-      }
-    }
-    e2s[rb * VC + v] = e2p;
-    zns[rb * VC + v] = znp;
-    if (rb == 0) e2s[8 * VC + v] = yn;
-  }
-  __syncthreads();
-  // contiguous write-out of the chunk's rows (un-padding the staged strides)
-  {
-    float2* zo = reinterpret_cast<float2*>(a.zq + g0 * NPP);
-    float* to = a.thrg + g0 * N4;
-    const int nwarps = nth >> 5;
-    for (int vv = warp; vv < vce; vv += nwarps) {
-      if (lane < 2 * NPP) zo[vv * 2 * NPP + lane] = zst[vv * (2 * NPP + 1) + lane];
-      if (lane < N4) to[vv * N4 + lane] = tst[vv * (N4 + 1) + lane];
-    }
-  }
-  for (int vv = tid; vv < vce; vv += nth) {
-    double e2 = 0.0, zn = 0.0;
-#pragma unroll
-    for (int w = 0; w < NRB; ++w) { e2 += e2s[w * VC + vv]; zn += zns[w * VC + vv]; }
-    const double yn = e2s[8 * VC + vv];
-    a.vaux[g0 + vv] = make_float2((float)sqrt(e2) * 1.001f, (float)(yn - zn));
-  }
-}
-
-// ===========================================================================
 // K2: partial-layer selection lists
 // ===========================================================================
 // K2 (templated on the expansion count E of the partial layer): one thread per
@@ -689,48 +546,24 @@ __device__ __forceinline__ void se_order(float x, int (&lev)[L], float (&d)[L]) 
   }
 }
 
-template <int N, int L, int EMAX>
-__global__ void __launch_bounds__(128)
-select_kernel(const DetectArgs a, const TreeParams tp, int pos, int npar, int vblocks) {
-  const int E = tp.e[pos];   // <= EMAX
-  constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
-  constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
+// The E nearest points (E <= EMAX) of the centre (xl, yl) in level-index units
+// (unclamped): packed label bytes (ir << 3 | ii) in `words`, the E-th and
+// (E+1)-th smallest squared distances (index units) in kprev / knext.  th =
+// the thread's slot in the per-thread shared-memory arrays (L = 8, EMAX > 4).
+template <int L, int EMAX>
+__device__ __forceinline__ void select_nearest(float xl, float yl, int E, int th,
+                                               unsigned (&words)[(EMAX + 3) / 4], float& kprev,
+                                               float& knext) {
   const float INF = __int_as_float(0x7f800000);
-  // grid.x = channel x vector block, grid.y = parent block: no per-thread division
-  const int c = blockIdx.x / vblocks;
-  const int vi = (blockIdx.x - c * vblocks) * blockDim.y + threadIdx.y;
-  const int par = blockIdx.y * blockDim.x + threadIdx.x;
-  if (par >= npar || vi >= a.V) return;
-  const int64_t gv = (int64_t)c * a.V + vi;
-  const float* tab = a.tables + (int64_t)c * TableLayout(a.m, N).total;
-  const TabPtrs T = tab_ptrs(tab, a.m, N);
-  const int p0 = par * tp.stride[pos + 1];
-  uint8_t* vlist = a.lists + gv * tp.list_bytes;
-  const float thr_pos = __ldg(a.thrg + gv * N4 + pos);   // issued early (used by the guard)
-  // acc of row pos after the expanded layers above it (the traversal's fma order)
-  const float2 z = reinterpret_cast<const float2*>(a.zq + gv * NPP)[pos];
-  float xr = z.x, xi = z.y;
-#pragma unroll
-  for (int q = 0; q < XM; ++q) {
-    const int j = N - 1 - q;
-    if (j > pos) {
-      int ir, ii;
-      expanded_symbol<L>(tp, j, p0, vlist, ir, ii);
-      const float2 r2 = rcol_at(T.rcol, NPP, pos, j);
-      acc_step(xr, xi, r2.x, r2.y, (float)ir, (float)ii);
-    }
-  }
-  const float kx = T.lay4[pos].x;
-  const float Eb = 0.5f - thr_pos;   // index-domain centre error bound
   int ox[L], oy[L];
   float dx[L], dy[L];
-  se_order<L>(__fmul_rn(xr, kx), ox, dx);
-  se_order<L>(__fmul_rn(xi, kx), oy, dy);
+  se_order<L>(xl, ox, dx);
+  se_order<L>(yl, oy, dy);
   constexpr int NW = (EMAX + 3) / 4;
-  unsigned words[NW];
 #pragma unroll
   for (int i = 0; i < NW; ++i) words[i] = 0u;
-  float kprev = 0.f, knext = 0.f;
+  kprev = 0.f;
+  knext = 0.f;
   if constexpr (EMAX <= 4) {
     // E <= 4: the E + 1 smallest sums lie in row 0, column 0 or at (1,1)
     // ((i+1)(j+1) <= 5): a two-pointer merge of row 0 and column 0 plus the corner
@@ -770,59 +603,64 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos, int npar, int vb
       ct = ct || (!ta && !tb);
     }
   } else {
-  int w[L];
-  float nk[L];
+    int w[L];
+    float nk[L];
 #pragma unroll
-  for (int i = 0; i < L; ++i) { w[i] = 0; nk[i] = dx[i] + dy[0]; }
-  // L = 8: the per-axis orders live in per-thread (transposed) shared memory,
-  // so the merge's data-dependent lookups are single LDS instead of select chains
-  constexpr bool SMEM = L == 8;
-  __shared__ float sdx[SMEM ? L : 1][128], sdy[SMEM ? L : 1][128];
-  __shared__ uint8_t sox[SMEM ? L : 1][128], soy[SMEM ? L : 1][128], sw[SMEM ? L : 1][128];
-  const int th = threadIdx.y * blockDim.x + threadIdx.x;
-  if (SMEM) {
+    for (int i = 0; i < L; ++i) { w[i] = 0; nk[i] = dx[i] + dy[0]; }
+    // L = 8: the per-axis orders live in per-thread (transposed) shared memory,
+    // so the merge's data-dependent lookups are single LDS instead of select chains
+    constexpr bool SMEM = L == 8;
+    __shared__ float sdx[SMEM ? L : 1][128], sdy[SMEM ? L : 1][128];
+    __shared__ uint8_t sox[SMEM ? L : 1][128], soy[SMEM ? L : 1][128], sw[SMEM ? L : 1][128];
+    if (SMEM) {
 #pragma unroll
-    for (int i = 0; i < L; ++i) {
-      sdx[i][th] = dx[i]; sdy[i][th] = dy[i];
-      sox[i][th] = (uint8_t)ox[i]; soy[i][th] = (uint8_t)oy[i]; sw[i][th] = 0;
-    }
-  }
-#pragma unroll
-  for (int pick = 0; pick <= EMAX; ++pick) {
-    if (pick > E) break;
-    int sel = 0;
-    float best = nk[0];
-#pragma unroll
-    for (int i = 1; i < L; ++i) {
-      const bool lt = nk[i] < best;
-      best = lt ? nk[i] : best;
-      sel = lt ? i : sel;
-    }
-    if (pick < E) {
-      int col;
-      unsigned b;
-      float nxt;
-      if (SMEM) {
-        col = sw[sel][th];
-        b = ((unsigned)sox[sel][th] << 3) | (unsigned)soy[col][th];
-        nxt = (col + 1 < L) ? sdx[sel][th] + sdy[col + 1][th] : INF;
-        sw[sel][th] = (uint8_t)(col + 1);
-      } else {
-        col = dyn_at(w, sel);
-        b = (unsigned)((dyn_at(ox, sel) << 3) | dyn_at(oy, col));
-        nxt = (col + 1 < L) ? dyn_at(dx, sel) + dyn_at(dy, col + 1) : INF;
+      for (int i = 0; i < L; ++i) {
+        sdx[i][th] = dx[i]; sdy[i][th] = dy[i];
+        sox[i][th] = (uint8_t)ox[i]; soy[i][th] = (uint8_t)oy[i]; sw[i][th] = 0;
       }
-      words[pick >> 2] |= b << (8 * (pick & 3));
-      kprev = best;
+    }
 #pragma unroll
-      for (int i = 0; i < L; ++i)
-        if (i == sel) { if (!SMEM) w[i] = col + 1; nk[i] = nxt; }
-    } else {
-      knext = best;
+    for (int pick = 0; pick <= EMAX; ++pick) {
+      if (pick > E) break;
+      int sel = 0;
+      float best = nk[0];
+#pragma unroll
+      for (int i = 1; i < L; ++i) {
+        const bool lt = nk[i] < best;
+        best = lt ? nk[i] : best;
+        sel = lt ? i : sel;
+      }
+      if (pick < E) {
+        int col;
+        unsigned b;
+        float nxt;
+        if (SMEM) {
+          col = sw[sel][th];
+          b = ((unsigned)sox[sel][th] << 3) | (unsigned)soy[col][th];
+          nxt = (col + 1 < L) ? sdx[sel][th] + sdy[col + 1][th] : INF;
+          sw[sel][th] = (uint8_t)(col + 1);
+        } else {
+          col = dyn_at(w, sel);
+          b = (unsigned)((dyn_at(ox, sel) << 3) | dyn_at(oy, col));
+          nxt = (col + 1 < L) ? dyn_at(dx, sel) + dyn_at(dy, col + 1) : INF;
+        }
+        words[pick >> 2] |= b << (8 * (pick & 3));
+        kprev = best;
+#pragma unroll
+        for (int i = 0; i < L; ++i)
+          if (i == sel) { if (!SMEM) w[i] = col + 1; nk[i] = nxt; }
+      } else {
+        knext = best;
+      }
     }
   }
-  }
-  uint8_t* out = vlist + tp.list_off[pos] + par * E;
+}
+
+// write E label bytes of one parent's selection
+template <int EMAX>
+__device__ __forceinline__ void store_selection(uint8_t* out, int E,
+                                                const unsigned (&words)[(EMAX + 3) / 4]) {
+  constexpr int NW = (EMAX + 3) / 4;
   if ((E & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
 #pragma unroll
     for (int i = 0; i < NW; ++i)
@@ -832,10 +670,223 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos, int npar, int vb
     for (int k = 0; k < EMAX; ++k)
       if (k < E) out[k] = (uint8_t)(words[k >> 2] >> (8 * (k & 3)));
   }
-  // cut guard: distance keys are within 2 sqrt2 E (sqrt k) + 2E^2 (+ rounding)
+}
+
+// cut guard: distance keys are within 2 sqrt2 E (sqrt k) + 2E^2 (+ rounding)
+__device__ __forceinline__ bool cut_near(float kprev, float knext, float Eb) {
   const float bound = 2.8284272f * Eb * (sqrt_up(kprev) + sqrt_up(knext)) + 4.f * Eb * Eb +
                       8.f * MPNL_U * (knext + 1.f);
-  if (knext - kprev <= bound) log_event(a, make_int4(p0, pos, (int)gv, EV_CUT));
+  return knext - kprev <= bound;
+}
+
+template <int N, int L, int EMAX>
+__global__ void __launch_bounds__(128)
+select_kernel(const DetectArgs a, const TreeParams tp, int pos, int npar, int vblocks) {
+  const int E = tp.e[pos];   // <= EMAX
+  constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
+  constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
+  // grid.x = channel x vector block, grid.y = parent block: no per-thread division
+  const int c = blockIdx.x / vblocks;
+  const int vi = (blockIdx.x - c * vblocks) * blockDim.y + threadIdx.y;
+  const int par = blockIdx.y * blockDim.x + threadIdx.x;
+  if (par >= npar || vi >= a.V) return;
+  const int64_t gv = (int64_t)c * a.V + vi;
+  const float* tab = a.tables + (int64_t)c * TableLayout(a.m, N).total;
+  const TabPtrs T = tab_ptrs(tab, a.m, N);
+  const int p0 = par * tp.stride[pos + 1];
+  uint8_t* vlist = a.lists + gv * tp.list_bytes;
+  const float thr_pos = __ldg(a.thrg + gv * N4 + pos);   // issued early (used by the guard)
+  // acc of row pos after the expanded layers above it (the traversal's fma order)
+  const float2 z = reinterpret_cast<const float2*>(a.zq + gv * NPP)[pos];
+  float xr = z.x, xi = z.y;
+#pragma unroll
+  for (int q = 0; q < XM; ++q) {
+    const int j = N - 1 - q;
+    if (j > pos) {
+      int ir, ii;
+      expanded_symbol<L>(tp, j, p0, vlist, ir, ii);
+      const float2 r2 = rcol_at(T.rcol, NPP, pos, j);
+      acc_step(xr, xi, r2.x, r2.y, (float)ir, (float)ii);
+    }
+  }
+  const float kx = T.lay4[pos].x;
+  unsigned words[(EMAX + 3) / 4];
+  float kprev, knext;
+  select_nearest<L, EMAX>(__fmul_rn(xr, kx), __fmul_rn(xi, kx), E,
+                          threadIdx.y * blockDim.x + threadIdx.x, words, kprev, knext);
+  store_selection<EMAX>(vlist + tp.list_off[pos] + par * E, E, words);
+  if (cut_near(kprev, knext, 0.5f - thr_pos)) log_event(a, make_int4(p0, pos, (int)gv, EV_CUT));
+}
+
+// ===========================================================================
+// K1b': per-vector preparation fused with the partial-layer selection.
+// Thread = vector (CTA = 128 vectors of one channel).  The channel's fp64 Q^H
+// (transposed) and shifts are staged in shared memory and read as broadcasts;
+// each thread rotates its own y in fp64 in blocks of RB rows (y re-read from
+// L1), writes its z' row pairs, guard thresholds and (E_acc, corr) as
+// contiguous 16-byte stores, and then -- when the tree's only partial layer
+// sits at the top or right below a full top layer (every BASELINE config) --
+// selects that layer's E nearest points for each of its parents from the
+// fp32 z' it just produced, with the traversal's arithmetic (select_nearest).
+// ===========================================================================
+template <int N>
+struct Prep2Smem {
+  // qt | shift | lay | y rows of the CTA's vectors (odd stride: conflict-free per-thread reads)
+  __host__ __device__ static constexpr int ystride(int m) { return m | 1; }
+  __host__ __device__ static constexpr int bytes(int m, int vpc, int yb) {
+    return 16 * m * N + 16 * N + 16 * N + vpc * ystride(m) * yb;
+  }
+};
+
+template <int N, int L, int EMAX, int TPV>
+__global__ void __launch_bounds__(128)
+prep2_kernel(const DetectArgs a, const TreeParams tp, int chunks, int pos_sel) {
+  constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
+  // rows per block (even, a multiple of 4); thread j of a vector's TPV group
+  // rotates blocks j, j + TPV, ... and selects for parents j, j + TPV, ...
+  constexpr int RB = TPV == 1 ? (N < 8 ? N4 : 8) : 4;
+  constexpr int NB = (N + RB - 1) / RB;
+  constexpr int VPC = 128 / TPV;                     // vectors per CTA
+  extern __shared__ __align__(16) uint8_t psm2[];
+  const int m = a.m;
+  double2* qt = reinterpret_cast<double2*>(psm2);
+  double2* sh = qt + m * N;
+  float4* ly = reinterpret_cast<float4*>(sh + N);
+  const TableLayout tl(m, N);
+  const int64_t c = blockIdx.x / chunks;
+  const int j = threadIdx.x % TPV;
+  const int v = (blockIdx.x - (int)c * chunks) * VPC + threadIdx.x / TPV;
+  const float* tab = a.tables + c * (int64_t)tl.total;
+  const int sy = Prep2Smem<N>::ystride(m);
+  const int v0 = (blockIdx.x - (int)c * chunks) * VPC;
+  const int nvc = (int)min((int64_t)VPC, a.V - v0);
+  float2* ys32 = reinterpret_cast<float2*>(ly + N);
+  double2* ys64 = reinterpret_cast<double2*>(ly + N);
+  {
+    const double2* q = reinterpret_cast<const double2*>(tab + tl.off_qh);
+    for (int i = threadIdx.x; i < m * N; i += 128) qt[i] = q[i];
+    const double2* s2 = reinterpret_cast<const double2*>(tab + tl.off_shift);
+    const float4* l4 = reinterpret_cast<const float4*>(tab + tl.off_lay);
+    for (int i = threadIdx.x; i < N; i += 128) { sh[i] = s2[i]; ly[i] = l4[i]; }
+    // the CTA's y rows: one coalesced flat copy into the padded layout
+    // ((v, r) by a float reciprocal: exact for i < 2^13 >= VPC * m)
+    const int64_t g0 = (c * a.V + v0) * m;
+    const float rm = 1.f / (float)m;
+    for (int i = threadIdx.x; i < nvc * m; i += 128) {
+      const int vv = (int)(((float)i + 0.5f) * rm), r = i - vv * m;
+      if (a.y_f64) ys64[vv * sy + r] = reinterpret_cast<const double2*>(a.y)[g0 + i];
+      else ys32[vv * sy + r] = reinterpret_cast<const float2*>(a.y)[g0 + i];
+    }
+  }
+  __syncthreads();
+  const bool live = v < a.V;   // (whole TPV groups share liveness: shuffles stay in-group)
+  const int64_t gv = c * a.V + (live ? v : 0);
+  const int vl = live ? v - v0 : 0;
+  auto yat = [&](int r) -> double2 {
+    if (a.y_f64) return ys64[vl * sy + r];
+    const float2 f = ys32[vl * sy + r];
+    return make_double2(f.x, f.y);
+  };
+  // ||y|| (every thread of the group: the per-row bounds need it)
+  double yn = 0.0;
+  for (int r = 0; r < m; ++r) {
+    const double2 y = yat(r);
+    yn = fma(y.x, y.x, fma(y.y, y.y, yn));
+  }
+  const float ynf = (float)sqrt(yn) * 1.0001f;
+  float4* zo = a.zq + gv * NPP;
+  float4* to = reinterpret_cast<float4*>(a.thrg + gv * N4);
+  double e2 = 0.0, zn = 0.0;
+  float zsr = 0.f, zsi = 0.f, thsel = 0.f;
+#pragma unroll
+  for (int b0 = 0; b0 < NB; b0 += TPV) {
+    const int k0 = (b0 + j) * RB;
+    if (k0 < N) {
+      double zr[RB], zi[RB];
+#pragma unroll
+      for (int t = 0; t < RB; ++t) { zr[t] = 0.0; zi[t] = 0.0; }
+      for (int r = 0; r < m; ++r) {
+        const double2 y = yat(r);
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+          if (k0 + t < N) {
+            const double2 q = qt[r * N + k0 + t];
+            zr[t] = fma(q.x, y.x, zr[t]);
+            zr[t] = fma(-q.y, y.y, zr[t]);
+            zi[t] = fma(q.x, y.y, zi[t]);
+            zi[t] = fma(q.y, y.x, zi[t]);
+          }
+        }
+      }
+      float zf[2 * RB], th[RB];
+#pragma unroll
+      for (int t = 0; t < RB; ++t) {
+        const int k = k0 + t;
+        zf[2 * t] = 0.f; zf[2 * t + 1] = 0.f; th[t] = 0.5f;
+        if (k < N) {
+          const double2 shk = sh[k];
+          const float2 z = make_float2((float)(zr[t] - shk.x), (float)(zi[t] - shk.y));
+          zf[2 * t] = z.x; zf[2 * t + 1] = z.y;
+          const float4 lk = ly[k];
+          const float e = row_bound(ynf, z, lk, k, m, N, L, a.guard_scale, 0);
+          th[t] = 0.5f - e / lk.y - MPNL_U * 3.f * L;
+          e2 += (double)e * e;
+          zn += zr[t] * zr[t] + zi[t] * zi[t];
+          if (k == pos_sel) { zsr = z.x; zsi = z.y; thsel = th[t]; }
+        }
+      }
+      if (live) {
+#pragma unroll
+        for (int q = 0; q < RB / 2; ++q)
+          if (k0 / 2 + q < NPP)
+            zo[k0 / 2 + q] = make_float4(zf[4 * q], zf[4 * q + 1], zf[4 * q + 2], zf[4 * q + 3]);
+#pragma unroll
+        for (int q = 0; q < RB / 4; ++q)
+          if (k0 + 4 * q < N4)
+            to[k0 / 4 + q] = make_float4(th[4 * q], th[4 * q + 1], th[4 * q + 2], th[4 * q + 3]);
+      }
+    }
+  }
+  if (TPV > 1) {
+    // group sums (fixed xor order) and the selected row from its owner thread
+#pragma unroll
+    for (int o = 1; o < TPV; o <<= 1) {
+      e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+      zn += __shfl_xor_sync(0xffffffffu, zn, o);
+    }
+    if (EMAX > 0 && pos_sel >= 0) {
+      const int src = (threadIdx.x & 31 & ~(TPV - 1)) + (pos_sel / RB) % TPV;
+      zsr = __shfl_sync(0xffffffffu, zsr, src);
+      zsi = __shfl_sync(0xffffffffu, zsi, src);
+      thsel = __shfl_sync(0xffffffffu, thsel, src);
+    }
+  }
+  if (!live) return;
+  if (j == 0) a.vaux[gv] = make_float2((float)sqrt(e2) * 1.001f, (float)(yn - zn));
+  if constexpr (EMAX > 0) {
+    // partial layer pos_sel: parents = the full top layer's L^2 points (or one
+    // parent when pos_sel is the top layer); centre of parent (ir, ii) =
+    // z'_pos + r''_{pos,N-1} (ir, ii) with the traversal's fma sequence
+    const int E = tp.e[pos_sel];
+    const int npar = pos_sel == N - 1 ? 1 : L * L;
+    const float kx = ly[pos_sel].x;
+    const float Eb = 0.5f - thsel;
+    const float2 r2 = pos_sel == N - 1 ? make_float2(0.f, 0.f)
+                                       : rcol_at(tab + tl.off_rcol, NPP, pos_sel, N - 1);
+    uint8_t* out = a.lists + gv * tp.list_bytes + tp.list_off[pos_sel];
+    const int st = tp.stride[pos_sel + 1];
+#pragma unroll 1
+    for (int par = j; par < npar; par += TPV) {
+      float xr = zsr, xi = zsi;
+      if (npar > 1) acc_step(xr, xi, r2.x, r2.y, (float)(par / L), (float)(par % L));
+      unsigned words[(EMAX + 3) / 4];
+      float kprev, knext;
+      select_nearest<L, EMAX>(__fmul_rn(xr, kx), __fmul_rn(xi, kx), E, threadIdx.x, words, kprev,
+                              knext);
+      store_selection<EMAX>(out + par * E, E, words);
+      if (cut_near(kprev, knext, Eb)) log_event(a, make_int4(par * st, pos_sel, (int)gv, EV_CUT));
+    }
+  }
 }
 
 // ===========================================================================

@@ -11,7 +11,7 @@
 namespace mpnl {
 
 // kind 0 = select_kernel (extra = layer), 1 = traverse_kernel, 2 = verify_kernel,
-// 3 = check_kernel, 4 = prep_kernel
+// 3 = check_kernel, 5 = prep2_kernel (fused prep + top selection)
 template <int NN, int L>
 cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp, unsigned grid,
                             int threads, size_t smem, int extra, cudaStream_t st) {
@@ -44,10 +44,24 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
       grid = (unsigned)std::min<long long>((long long)std::max(nb, 1) * sms, (long long)extra);
     }
     k<<<grid, threads, smem, st>>>(a, tp);
-  } else if (kind == 4) {
-    auto k = prep_kernel<NN, L>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, threads, smem, st>>>(a, tp, extra);
+  } else if (kind == 5) {
+    // fused prep + top partial-layer selection (E <= 4); extra = pos_sel (-1:
+    // none), threads = threads per vector (1, or 4 for small batches)
+    const int pos = extra;
+    const int tpv = threads == 4 ? 4 : 1;
+    const int sm = Prep2Smem<NN>::bytes(a.m, 128 / tpv, a.y_f64 ? 16 : 8);
+    const int chunks = (int)((a.V + 128 / tpv - 1) / (128 / tpv));
+    auto launch = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      kern<<<(unsigned)(a.n_ch * chunks), 128, sm, st>>>(a, tp, chunks, pos);
+    };
+    if (tpv == 1) {
+      if (pos < 0) launch(prep2_kernel<NN, L, 0, 1>);
+      else launch(prep2_kernel<NN, L, 4, 1>);
+    } else {
+      if (pos < 0) launch(prep2_kernel<NN, L, 0, 4>);
+      else launch(prep2_kernel<NN, L, 4, 4>);
+    }
   } else if (kind == 2) {
     verify_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
   } else {
