@@ -364,7 +364,7 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
       const int64_t vb = (B + 127) / 128;
       e = launch_fast(n, L, 2, a, tp, (unsigned)vb, 128, 0, 0, st);
       if (e != cudaSuccess) return cuda_fail(e, "verify kernel");
-      const int64_t cb = std::min<int64_t>(std::max<int64_t>((B + 255) / 256, 1), 148 * 16);
+      const int64_t cb = 148 * 16;   // capped at the resident capacity by the launcher
       e = launch_fast(n, L, 3, a, tp, (unsigned)cb, 128, 0, 0, st);
       if (e != cudaSuccess) return cuda_fail(e, "check kernel");
     }
