@@ -319,7 +319,8 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     int fused = -1;
     for (int pos = n - 1; pos >= n - tp.n_top; --pos) {
       if (tp.e[pos] == L * L) continue;
-      if (tp.e[pos] <= 4 && (pos == n - 1 || (pos == n - 2 && tp.e[n - 1] == L * L)))
+      if ((tp.e[pos] == 2 || tp.e[pos] == 4) &&
+          (pos == n - 1 || (pos == n - 2 && tp.e[n - 1] == L * L)))
         fused = pos;
       break;
     }

@@ -656,6 +656,75 @@ __device__ __forceinline__ void select_nearest(float xl, float yl, int E, int th
   }
 }
 
+// first K entries of the per-axis Schnorr-Euchner order (levels by distance
+// to x, ties to the lower level), K <= L
+template <int L, int K>
+__device__ __forceinline__ void se_order_k(float x, int (&lev)[K], float (&d)[K]) {
+  const int n0 = (int)rintf(fminf(fmaxf(x, 0.f), (float)(L - 1)));
+  int lo = n0 - 1, hi = n0 + 1;
+  lev[0] = n0;
+  d[0] = (x - n0) * (x - n0);
+#pragma unroll
+  for (int r = 1; r < K; ++r) {
+    const bool up = (hi < L) && (lo < 0 || (hi - x) < (x - lo));
+    const int l = up ? hi : lo;
+    hi += up ? 1 : 0;
+    lo -= up ? 0 : 1;
+    lev[r] = l;
+    d[r] = (x - l) * (x - l);
+  }
+}
+
+// select_nearest for a compile-time E <= 4: the same two-pointer merge of
+// row 0 / column 0 / corner (1,1), fully unrolled (no E-dependent branches)
+// over only the min(L, E + 1) leading entries of each axis order.
+template <int L, int E>
+__device__ __forceinline__ void select_nearest_e(float xl, float yl, unsigned& word, float& kprev,
+                                                 float& knext) {
+  static_assert(E >= 2 && E <= 4, "E in 2..4");
+  constexpr int KK = (E + 1) < L ? (E + 1) : L;   // entries per axis
+  constexpr int K = KK - 1;                        // row-0 / column-0 candidates
+  const float INF = __int_as_float(0x7f800000);
+  int ox[KK], oy[KK];
+  float dx[KK], dy[KK];
+  se_order_k<L, KK>(xl, ox, dx);
+  se_order_k<L, KK>(yl, oy, dy);
+  float ra[K], cb[K];
+  unsigned la[K], lb[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    ra[t] = dx[0] + dy[t + 1];
+    cb[t] = dx[t + 1] + dy[0];
+    la[t] = ((unsigned)ox[0] << 3) | (unsigned)oy[t + 1];
+    lb[t] = ((unsigned)ox[t + 1] << 3) | (unsigned)oy[0];
+  }
+  const float cc = dx[1] + dy[1];
+  const unsigned lc = ((unsigned)ox[1] << 3) | (unsigned)oy[1];
+  word = ((unsigned)ox[0] << 3) | (unsigned)oy[0];
+  kprev = dx[0] + dy[0];
+  knext = INF;
+  int i = 0, j = 0;
+  bool ct = false;
+#pragma unroll
+  for (int k = 1; k <= E; ++k) {
+    const float va = i < K ? dyn_at(ra, i) : INF;
+    const float vb = j < K ? dyn_at(cb, j) : INF;
+    const float vc = (i >= 1 && j >= 1 && !ct) ? cc : INF;
+    const bool ta = va <= vb && va <= vc, tb = !ta && vb <= vc;
+    const float v = ta ? va : (tb ? vb : vc);
+    if (k < E) {
+      const unsigned b = ta ? dyn_at(la, i) : (tb ? dyn_at(lb, j) : lc);
+      word |= b << (8 * k);
+      kprev = v;
+    } else {
+      knext = v;
+    }
+    i += ta ? 1 : 0;
+    j += tb ? 1 : 0;
+    ct = ct || (!ta && !tb);
+  }
+}
+
 // write E label bytes of one parent's selection
 template <int EMAX>
 __device__ __forceinline__ void store_selection(uint8_t* out, int E,
@@ -738,7 +807,7 @@ struct Prep2Smem {
   }
 };
 
-template <int N, int L, int EMAX, int TPV>
+template <int N, int L, int E, int TPV>
 __global__ void __launch_bounds__(128)
 prep2_kernel(const DetectArgs a, const TreeParams tp, int chunks, int pos_sel) {
   constexpr int NPP = (N + 1) / 2, N4 = (N + 3) & ~3;
@@ -854,7 +923,7 @@ prep2_kernel(const DetectArgs a, const TreeParams tp, int chunks, int pos_sel) {
       e2 += __shfl_xor_sync(0xffffffffu, e2, o);
       zn += __shfl_xor_sync(0xffffffffu, zn, o);
     }
-    if (EMAX > 0 && pos_sel >= 0) {
+    if (E > 0 && pos_sel >= 0) {
       const int src = (threadIdx.x & 31 & ~(TPV - 1)) + (pos_sel / RB) % TPV;
       zsr = __shfl_sync(0xffffffffu, zsr, src);
       zsi = __shfl_sync(0xffffffffu, zsi, src);
@@ -863,11 +932,11 @@ prep2_kernel(const DetectArgs a, const TreeParams tp, int chunks, int pos_sel) {
   }
   if (!live) return;
   if (j == 0) a.vaux[gv] = make_float2((float)sqrt(e2) * 1.001f, (float)(yn - zn));
-  if constexpr (EMAX > 0) {
-    // partial layer pos_sel: parents = the full top layer's L^2 points (or one
-    // parent when pos_sel is the top layer); centre of parent (ir, ii) =
-    // z'_pos + r''_{pos,N-1} (ir, ii) with the traversal's fma sequence
-    const int E = tp.e[pos_sel];
+  if constexpr (E > 0) {
+    // partial layer pos_sel (tp.e[pos_sel] == E): parents = the full top
+    // layer's L^2 points (or one parent when pos_sel is the top layer); centre
+    // of parent (ir, ii) = z'_pos + r''_{pos,N-1} (ir, ii) with the traversal's
+    // fma sequence
     const int npar = pos_sel == N - 1 ? 1 : L * L;
     const float kx = ly[pos_sel].x;
     const float Eb = 0.5f - thsel;
@@ -879,11 +948,15 @@ prep2_kernel(const DetectArgs a, const TreeParams tp, int chunks, int pos_sel) {
     for (int par = j; par < npar; par += TPV) {
       float xr = zsr, xi = zsi;
       if (npar > 1) acc_step(xr, xi, r2.x, r2.y, (float)(par / L), (float)(par % L));
-      unsigned words[(EMAX + 3) / 4];
+      unsigned word;
       float kprev, knext;
-      select_nearest<L, EMAX>(__fmul_rn(xr, kx), __fmul_rn(xi, kx), E, threadIdx.x, words, kprev,
-                              knext);
-      store_selection<EMAX>(out + par * E, E, words);
+      select_nearest_e<L, E>(__fmul_rn(xr, kx), __fmul_rn(xi, kx), word, kprev, knext);
+      if (E == 4) {
+        *reinterpret_cast<unsigned*>(out + par * 4) = word;
+      } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) out[par * E + k] = (uint8_t)(word >> (8 * k));
+      }
       if (cut_near(kprev, knext, Eb)) log_event(a, make_int4(par * st, pos_sel, (int)gv, EV_CUT));
     }
   }
@@ -1052,6 +1125,16 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   const int it_end = (int)((int64_t)(blockIdx.x + 1) * I / gridDim.x);
   const TabPtrs T = tab_ptrs(tab, a.m, N);
 
+#ifdef MPNL_SKEW_NS
+  // co-resident CTAs (b, b + G/k, ...) start out of phase: their warps share
+  // the SM sub-partitions and would otherwise hit the update-heavy top layers
+  // and the latency-bound bottom layers in lockstep
+  {
+    int nsm = 148;
+    const int slot = (int)(blockIdx.x / (unsigned)nsm);
+    if (slot) __nanosleep((unsigned)(slot * MPNL_SKEW_NS));
+  }
+#endif
   for (int seg = it_begin; seg < it_end;) {
     const int c = seg / ipc;
     const int ibase = c * ipc, vbase = c * V;

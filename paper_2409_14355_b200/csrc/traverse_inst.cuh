@@ -45,7 +45,7 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
     }
     k<<<grid, threads, smem, st>>>(a, tp);
   } else if (kind == 5) {
-    // fused prep + top partial-layer selection (E <= 4); extra = pos_sel (-1:
+    // fused prep + top partial-layer selection (E = 2 or 4); extra = pos_sel (-1:
     // none), threads = threads per vector (1, or 4 for small batches)
     const int pos = extra;
     const int tpv = threads == 4 ? 4 : 1;
@@ -55,11 +55,14 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       kern<<<(unsigned)(a.n_ch * chunks), 128, sm, st>>>(a, tp, chunks, pos);
     };
+    const int e = pos >= 0 ? tp.e[pos] : 0;   // 0, 2 or 4 (abi.cu)
     if (tpv == 1) {
-      if (pos < 0) launch(prep2_kernel<NN, L, 0, 1>);
+      if (e == 0) launch(prep2_kernel<NN, L, 0, 1>);
+      else if (e == 2) launch(prep2_kernel<NN, L, 2, 1>);
       else launch(prep2_kernel<NN, L, 4, 1>);
     } else {
-      if (pos < 0) launch(prep2_kernel<NN, L, 0, 4>);
+      if (e == 0) launch(prep2_kernel<NN, L, 0, 4>);
+      else if (e == 2) launch(prep2_kernel<NN, L, 2, 4>);
       else launch(prep2_kernel<NN, L, 4, 4>);
     }
   } else if (kind == 2) {
