@@ -195,3 +195,27 @@ def test_host_pipeline_equals_device_path(name, n_rb, chunk):
     hd, md = det.mpnl_detect_hard(plan, h.cuda(), y.cuda(), c)
     assert torch.equal(hd.cpu(), hard)
     assert torch.equal(md.cpu(), metric)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5P16", "C5P256"])
+def test_large_batch_tiled_golden(name):
+    """The golden RBs tiled into a batch of >= 151,552 vectors, which takes the
+    large-batch kernel variants (one prep thread per vector, fused selection):
+    every copy must reproduce the reference golden."""
+    import torch
+    det = _det()
+    g = np.load(GOLD / f"hard_{name}.npz")
+    cfg = CONFIGS[name]
+    c = constellation_for(cfg.order)
+    n_ch, V = g["y"].shape[:2]
+    reps = -(-151552 // (n_ch * V))
+    h = torch.from_numpy(np.ascontiguousarray(g["h"])).cuda().repeat(reps, 1, 1)
+    y = torch.from_numpy(np.ascontiguousarray(g["y"])).cuda().repeat(reps, 1, 1)
+    plan = det.mpnl_plan_batch(h, float(g["nv"]), int(g["n_paths"]), c)
+    hard, metric = det.mpnl_detect_hard(plan, h, y, c)
+    hard = hard.cpu().numpy().reshape(reps, n_ch, V, -1)
+    metric = metric.cpu().numpy().reshape(reps, n_ch, V)
+    for r in (0, reps // 2, reps - 1):
+        _check_hard(hard[r].astype(np.int64), metric[r].astype(np.float64), g["hard"], g["m1"],
+                    g["m2"], f"{name} tile {r}")
+    assert (hard == hard[:1]).all() and (metric == metric[:1]).all()
