@@ -299,16 +299,20 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
     double bm = CUDART_INF;
     int bp = 0x7fffffff;
     unsigned long long bk[3] = {~0ull, ~0ull, ~0ull};
+    // (rolled loops, residuals in local memory: the kernel runs for a few
+    // vectors, so its cold instruction fetch, not its arithmetic, sets the
+    // latency -- keep the code small)
     for (int p = tid; p < P; p += EX_THREADS) {
       double2 acc[N];
-#pragma unroll
+#pragma unroll 1
       for (int k = 0; k < N; ++k) acc[k] = make_double2(0.0, 0.0);
       unsigned long long key[3] = {0ull, 0ull, 0ull};
       double ped = 0.0, xs2 = 0.0;
-#pragma unroll
+#pragma unroll 1
       for (int pos = N - 1; pos >= 0; --pos) {
         const double rpp = Rs[pos * N + pos].x;
-        const double ur = zs[pos].x - acc[pos].x, ui = zs[pos].y - acc[pos].y;
+        const double2 ap = acc[pos];
+        const double ur = zs[pos].x - ap.x, ui = zs[pos].y - ap.y;
         const int e = tp.e[pos];
         int ir, ii;
         if (e == 1) {
@@ -334,11 +338,13 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
         key[1] |= (w == 1) ? (unsigned long long)lab << sh : 0ull;
         key[2] |= (w == 2) ? (unsigned long long)lab << sh : 0ull;
         if (a.full_labels) a.full_labels[(gv * P + p) * N + k] = (uint8_t)lab;
-#pragma unroll
+#pragma unroll 2
         for (int kk = 0; kk < pos; ++kk) {
           const double2 r = Rs[kk * N + pos];
-          acc[kk].x = fma(r.x, sr, fma(-r.y, si, acc[kk].x));
-          acc[kk].y = fma(r.x, si, fma(r.y, sr, acc[kk].y));
+          double2 v = acc[kk];
+          v.x = fma(r.x, sr, fma(-r.y, si, v.x));
+          v.y = fma(r.x, si, fma(r.y, sr, v.y));
+          acc[kk] = v;
         }
       }
       double met = ped + c0;
