@@ -274,7 +274,9 @@ __device__ __forceinline__ void guard_mark(float d, float th, unsigned bit, floa
 // zs: per vector NPP float4 {re_2q, im_2q, re_2q+1, im_2q+1}.
 // LAB (NS == 1): record level indices lab[pos] and PED prefix pre[pos] and
 // stop after layer `stop` (phase re-traces).
-template <int N, int L, int NS, bool GUARD, bool LAB, bool SAMEV = false>
+// SH (NS == 2): the lane's two paths are siblings under the top layer (same
+// top symbol): the top layer's PED term and row updates are computed once.
+template <int N, int L, int NS, bool GUARD, bool LAB, bool SAMEV = false, bool SH = false>
 __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* __restrict__ zs,
                                                const float* __restrict__ thr,
                                                const uint8_t* __restrict__ lists,
@@ -354,8 +356,12 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
       pre[pos] = lo32(ped2[0]) + hi32(ped2[0]);
       if (pos == stop) return;
     }
+    constexpr bool SH2 = SH && NS == 2;
+    const bool shared = SH2 && pos == N - 1;   // compile-time in the unrolled loop
+    const int ns = shared ? 1 : NS;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
+      if (s >= ns) break;
       const u64 e2 = ffma2(pk2(-c2r, -c2r), g2[s], acc[s][pos]);   // c2r n + u
       ped2[s] = ffma2(e2, e2, ped2[s]);
     }
@@ -366,6 +372,7 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
       const float4 r = rc[q];              // {rr_2q, ri_2q, rr_2q+1, ri_2q+1}
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
+        if (s >= ns) break;
         const u64 gs = pk2(-hi32(g2[s]), lo32(g2[s]));   // (fi, -fr): operand modifiers
         acc[s][2 * q] = ffma2(pk2(-r.x, -r.x), g2[s], acc[s][2 * q]);
         acc[s][2 * q] = ffma2(gs, pk2(-r.y, -r.y), acc[s][2 * q]);
@@ -374,6 +381,11 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
           acc[s][2 * q + 1] = ffma2(gs, pk2(-r.w, -r.w), acc[s][2 * q + 1]);
         }
       }
+    }
+    if (shared) {   // the sibling continues from the shared state (register renaming)
+#pragma unroll
+      for (int k = 0; k < 2 * NPP; ++k) acc[NS - 1][k] = acc[0][k];
+      ped2[NS - 1] = ped2[0];
     }
   }
 #pragma unroll
@@ -1057,7 +1069,9 @@ __device__ __forceinline__ void trav_issue(const DetectArgs& a, const TravSmem& 
 // VPI = false: one vector per item, its P paths in bpv batches of 32 PT paths
 //              (every path of a lane is on the same vector);
 // VPI = true : vpi = 32 PT / P vectors per item, one batch.
-template <int N, int L, bool VPI>
+// SH: (non-VPI, PT = 2) lane l holds the sibling paths 2l, 2l + 1 of a batch
+// (same top symbol: requires an even top-layer stride), sharing the top layer.
+template <int N, int L, bool VPI, bool SH = false>
 __global__ void __launch_bounds__(TravCfg<N>::MAXT, TravCfg<N>::MINB)
 traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   constexpr int PT = TravCfg<N>::PT;
@@ -1098,7 +1112,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
 #pragma unroll
     for (int t = 0; t < PT; ++t) {
-      const int s = t * 32 + lane;
+      const int s = SH ? 2 * lane + t : t * 32 + lane;
       const int p = VPI ? s % P : s;
 #pragma unroll
       for (int j = 0; j < XM; ++j) {
@@ -1204,7 +1218,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         bool ok[PT];
 #pragma unroll
         for (int t = 0; t < PT; ++t) {
-          const int s = t * 32 + lane;
+          const int s = SH ? 2 * lane + t : t * 32 + lane;
           if (!VPI) {
             vl[t] = 0;
             pp[t] = b * S + s;
@@ -1219,7 +1233,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         }
         float ped[PT], evp[PT];
         unsigned evm[PT];
-        traverse_paths<N, L, PT, true, false, !VPI>(T, zs, thr, lch, tp, lbytes, vl, gvl, pp, ped,
+        traverse_paths<N, L, PT, true, false, !VPI, SH>(T, zs, thr, lch, tp, lbytes, vl, gvl, pp, ped,
                                                     evm, evp, nullptr, nullptr, -1,
                                                     use_xs ? xs : nullptr);
         if (!VPI) {   // running top-3; the event bound includes this batch's own best

@@ -34,7 +34,12 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
     }
   } else if (kind == 1) {
     // persistent: grid = resident capacity (capped by the item count `extra`)
-    auto k = a.vpi > 1 ? traverse_kernel<NN, L, true> : traverse_kernel<NN, L, false>;
+    // top-layer sharing of sibling path pairs (PT = 2, one vector per batch, even top stride)
+    constexpr bool CAN_SH = TravCfg<NN>::PT == 2;
+    const bool sh = CAN_SH && a.vpi <= 1 && tp.n_top >= 1 && tp.stride[NN - 1] % 2 == 0 &&
+                    tp.n_paths % 2 == 0;
+    auto k = a.vpi > 1 ? traverse_kernel<NN, L, true>
+                       : (sh ? traverse_kernel<NN, L, false, CAN_SH> : traverse_kernel<NN, L, false>);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (grid == 0) {
       int nb = 0, dev = 0, sms = 148;
