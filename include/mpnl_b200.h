@@ -14,6 +14,7 @@
  *                             (the hard-output composition of cli.py:236-239
  *                              and test_acceptance.py:114-117)
  *   mpnl_detect_full       <- mpnl_detect_batch      detect.py:473-488
+ *   mpnl_candidate_llrs    <- _candidate_llrs_batch  detect.py:439-453
  * INTEGRATION.md shows the ctypes binding a maintainer adds to detect.py.
  */
 #ifndef MPNL_B200_H
@@ -114,6 +115,19 @@ int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64,
                      const int64_t* expansions, double noise_var,
                      uint8_t* labels, double* metrics, int64_t* best,
                      void* stream);
+
+/* List max-log LLRs over a candidate list (replaces _candidate_llrs_batch,
+ * detect.py:439-453; bits as bits_from_labels, core.py:209-213, MSB first).
+ * labels (B, P, n) uint8 and metrics (B, P) float64 as mpnl_detect_full
+ * writes them (device); llr_out (B, n, log2 q) float64 (device).  noise_var
+ * is used when noise_var_per_vector is NULL, else that device float64 (B,)
+ * array is (the reference's array-valued noise_var).  Bit-identical to the
+ * reference: bits no path sets/clears saturate at +-clip.
+ * Errors: P < 1 -> MPNL_EINVAL ("empty candidate list"). */
+int mpnl_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t n_vectors,
+                        int64_t n_paths, int n, int q, double noise_var,
+                        const double* noise_var_per_vector, double clip, double* llr_out,
+                        void* stream);
 
 /* Scale of the fp32 error bound used by the traversal guard (default 1 =
  * the rigorous bound; <= 0 restores the default).  Diagnostics only. */

@@ -250,3 +250,25 @@ def detect_rb_parallel(h_rb, y_rb, noise_var, n_paths, order, workers=None,
         with ProcessPoolExecutor(max_workers=workers) as pool:
             parts = list(pool.map(_chunk_worker, tasks))
     return tuple(np.concatenate([p[i] for p in parts]) for i in range(3))
+
+
+# --------------------------------------------------------------------------
+# list max-log LLRs
+# --------------------------------------------------------------------------
+
+def candidate_llrs(labels, metrics, noise_var, order, clip=20.0):
+    """Max-log LLRs over candidate lists (detect.py:439-453): labels (B,P,N),
+    metrics (B,P) -> (B,N,bps) float64.  Bits MSB first as bits_from_labels
+    (core.py:209-213); clip = LLR_CLIP (core.py:21); noise_var scalar or (B,)."""
+    bps = int(order).bit_length() - 1
+    lab = np.asarray(labels, dtype=np.int64)
+    bits = ((lab[..., None] >> np.arange(bps - 1, -1, -1)) & 1).astype(bool)
+    mm = np.asarray(metrics, dtype=np.float64)[:, :, None, None]
+    min1 = np.where(bits, mm, np.inf).min(axis=1)
+    min0 = np.where(~bits, mm, np.inf).min(axis=1)
+    nv = np.asarray(noise_var, dtype=np.float64)
+    if nv.ndim:
+        nv = nv.reshape((-1,) + (1,) * (min0.ndim - 1))
+    with np.errstate(invalid="ignore"):
+        llr = (min1 - min0) / nv
+    return np.clip(llr, -clip, clip)

@@ -33,6 +33,9 @@ MPNL_DECL_PART(8, 0) MPNL_DECL_PART(8, 1) MPNL_DECL_PART(8, 2) MPNL_DECL_PART(8,
 
 namespace mpnl {
 cudaError_t launch_exact(const ExactArgs& a, const TreeParams& tp, int grid, cudaStream_t st);
+cudaError_t launch_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t B,
+                                  int64_t P, int n, int bps, double nv, const double* nv_vec,
+                                  double clip, double* llr, cudaStream_t st);
 }
 
 __global__ void flags_kernel(uint8_t* flags, const uint32_t* vflag, int64_t B, int all) {
@@ -454,6 +457,24 @@ int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64, con
   const int grid = (int)std::min<int64_t>(B, 148 * 8);
   cudaError_t e = launch_exact(ea, tb.tp, grid, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "exact kernel");
+  return MPNL_OK;
+}
+
+int mpnl_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t n_vectors,
+                        int64_t n_paths, int n, int q, double noise_var,
+                        const double* noise_var_per_vector, double clip, double* llr_out,
+                        void* stream) {
+  if (n_paths < 1) return fail(MPNL_EINVAL, "empty candidate list");
+  if (n < 1 || n_vectors < 0) return fail(MPNL_EINVAL, "inconsistent candidate list dimensions");
+  if (n > MPNL_MAX_N) return fail(MPNL_EUNSUPPORTED, "N > 32 streams is not supported");
+  const int L = levels_for(q);
+  if (!L) return fail(MPNL_EUNSUPPORTED, "unsupported constellation order " + std::to_string(q));
+  if (n_vectors == 0) return MPNL_OK;
+  const int bps = q == 4 ? 2 : (q == 16 ? 4 : 6);
+  cudaError_t e = launch_candidate_llrs(labels, metrics, n_vectors, n_paths, n, bps, noise_var,
+                                        noise_var_per_vector, clip, llr_out,
+                                        (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "candidate llr kernel");
   return MPNL_OK;
 }
 

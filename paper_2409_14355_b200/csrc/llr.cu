@@ -1,0 +1,111 @@
+// List max-log LLRs over a candidate list.
+//
+// Reference: `_candidate_llrs_batch` (pkg/src/mpnlsim/detect.py:439-453) with the
+// bit expansion of `bits_from_labels` (core.py:209-213, MSB first) and LLR_CLIP
+// (core.py:21).  Per vector b, stream n and bit j:
+//     min1 = min over paths with bit j of labels[b,p,n] set   of metrics[b,p]
+//     min0 = min over paths with the bit clear                of metrics[b,p]
+//     llr[b,n,j] = clip((min1 - min0) / nv_b, -clip, clip)
+// A bit no path sets (or clears) has min = +inf and saturates, exactly as
+// numpy does.  All arithmetic is one IEEE fp64 subtraction and one correctly
+// rounded fp64 division, so the result is bit-identical to the reference.
+//
+// Layout: labels (B, P, N) uint8, metrics (B, P) fp64, llr (B, N, bps) fp64 — the
+// mpnl_detect_full outputs as they sit in HBM.  The kernel is HBM-bound byte
+// work: one warp per vector, lane = stream, so every path is one coalesced
+// N-byte row read plus a broadcast metric; the 2·bps running minima live in
+// registers.  Grid: persistent warps strided over vectors.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mpnl {
+
+template <int BPS>
+__global__ void __launch_bounds__(256) candidate_llr_kernel(
+    const uint8_t* __restrict__ labels, const double* __restrict__ metrics, int64_t B,
+    int64_t P, int n, double nv, const double* __restrict__ nv_vec, double clip,
+    double* __restrict__ llr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool active = lane < n;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  for (int64_t b = warp; b < B; b += n_warps) {
+    double mn1[BPS], mn0[BPS];
+#pragma unroll
+    for (int j = 0; j < BPS; ++j) mn1[j] = mn0[j] = inf;
+    const uint8_t* lab = labels + b * P * n + lane;
+    const double* met = metrics + b * P;
+    int64_t p = 0;
+    for (; p + 4 <= P; p += 4) {
+      unsigned l4[4];
+      double m4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        l4[u] = active ? __ldg(lab + (p + u) * n) : 0u;
+        m4[u] = __ldg(met + p + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int j = 0; j < BPS; ++j) {
+          const bool bit = (l4[u] >> (BPS - 1 - j)) & 1u;
+          if (bit) mn1[j] = m4[u] < mn1[j] ? m4[u] : mn1[j];
+          else mn0[j] = m4[u] < mn0[j] ? m4[u] : mn0[j];
+        }
+      }
+    }
+    for (; p < P; ++p) {
+      const unsigned l = active ? __ldg(lab + p * n) : 0u;
+      const double m = __ldg(met + p);
+#pragma unroll
+      for (int j = 0; j < BPS; ++j) {
+        const bool bit = (l >> (BPS - 1 - j)) & 1u;
+        if (bit) mn1[j] = m < mn1[j] ? m : mn1[j];
+        else mn0[j] = m < mn0[j] ? m : mn0[j];
+      }
+    }
+    if (active) {
+      const double v = nv_vec ? nv_vec[b] : nv;
+      double* out = llr + (b * n + lane) * BPS;
+#pragma unroll
+      for (int j = 0; j < BPS; ++j) {
+        double x = __ddiv_rn(__dsub_rn(mn1[j], mn0[j]), v);
+        // np.clip: NaN stays NaN, otherwise min(max(x, -clip), clip)
+        if (x < -clip) x = -clip;
+        if (x > clip) x = clip;
+        out[j] = x;
+      }
+    }
+  }
+}
+
+cudaError_t launch_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t B,
+                                  int64_t P, int n, int bps, double nv, const double* nv_vec,
+                                  double clip, double* llr, cudaStream_t st) {
+  const int threads = 256;
+  const int64_t warps_needed = B;
+  int64_t blocks = (warps_needed + (threads / 32) - 1) / (threads / 32);
+  const int64_t cap = 148 * 8;  // 8 resident 256-thread CTAs per SM
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  switch (bps) {
+    case 2:
+      candidate_llr_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(labels, metrics, B, P, n,
+                                                                    nv, nv_vec, clip, llr);
+      break;
+    case 4:
+      candidate_llr_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(labels, metrics, B, P, n,
+                                                                    nv, nv_vec, clip, llr);
+      break;
+    case 6:
+      candidate_llr_kernel<6><<<(unsigned)blocks, threads, 0, st>>>(labels, metrics, B, P, n,
+                                                                    nv, nv_vec, clip, llr);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace mpnl

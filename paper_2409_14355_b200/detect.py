@@ -11,6 +11,8 @@ this module                reference                                   kernels
 allocate_expansions        detect.py:221-280                           host C++ port
 mpnl_plan_batch            detect.py:361-388 (+ _sorted_qr_batch)      K1 plan (fp64 QR)
 mpnl_detect_batch          detect.py:473-488 (full candidate list)     K5 exact (fp64)
+_candidate_llrs_batch      detect.py:439-453 (list max-log LLRs)       K6 candidate LLR
+mpnl_detect_llrs           linksim.py:151-155 (the "mpnl" branch)      K5 + K6 on device
 mpnl_detect_hard           hard composition cli.py:236-239,            K3 fp32 traversal +
                            test_acceptance.py:114-117                  K5 fix-up of flags
 mpnl_hard_output           plan + hard composition from HOST arrays    K1-K5, pipelined
@@ -44,7 +46,7 @@ __all__ = [
     "allocate_expansions", "BatchPathPlan", "PathPlan", "mpnl_plan_batch",
     "mpnl_preprocess", "mpnl_detect_batch", "mpnl_detect_hard", "mpnl_hard_output", "mpnl_detect",
     "detect", "DetectorInput", "CandidateList", "DetectionOutput",
-    "llr_from_candidates", "DETECTOR_NAMES", "SingularChannelError",
+    "llr_from_candidates", "mpnl_detect_llrs", "DETECTOR_NAMES", "SingularChannelError",
 ]
 
 
@@ -417,19 +419,70 @@ def _residual_metric(h, y, x):
     return float(np.real(np.vdot(r, r)))
 
 
+def _candidate_llrs_batch(labels, metrics, noise_var, c: Constellation,
+                          clip: float = LLR_CLIP):
+    """Max-log LLRs over candidate lists (detect.py:439-453) on the GPU.
+
+    labels (B, P, N) and metrics (B, P) — numpy (result numpy float64) or CUDA
+    tensors (uint8 / float64; result stays on the device).  `noise_var` is a
+    scalar or a per-row (B,) array, as in the reference.  Returns
+    (B, N, log2 Q) float64, bit-identical to the reference."""
+    lib = _lib.load()
+    was_np = not isinstance(labels, torch.Tensor)
+    dev = labels.device if not was_np else _device()
+    if was_np:
+        lab = np.asarray(labels)
+        if lab.size and (lab.min() < 0 or lab.max() >= c.order):
+            raise ValueError("labels outside the constellation")
+        lab_t = torch.from_numpy(np.ascontiguousarray(lab.astype(np.uint8))).to(dev)
+    else:
+        lab_t = labels.to(dev, torch.uint8).contiguous()
+    met_t = (torch.as_tensor(np.asarray(metrics, dtype=np.float64)) if not
+             isinstance(metrics, torch.Tensor) else metrics).to(dev, torch.float64).contiguous()
+    if lab_t.dim() != 3 or met_t.shape != lab_t.shape[:2]:
+        raise ValueError("labels must be (B, P, N) and metrics (B, P)")
+    b, p, n = lab_t.shape
+    nv_arr = np.asarray(noise_var.cpu() if isinstance(noise_var, torch.Tensor) else noise_var,
+                        dtype=np.float64)
+    nv_t = None
+    if nv_arr.ndim:
+        nv_t = torch.from_numpy(np.ascontiguousarray(nv_arr.reshape(-1))).to(dev)
+        if nv_t.numel() != b:
+            raise ValueError("noise_var must be a scalar or one value per candidate list")
+    llr = torch.empty((b, n, c.bits_per_symbol), dtype=torch.float64, device=dev)
+    rc = lib.mpnl_candidate_llrs(lab_t.data_ptr(), met_t.data_ptr(), b, p, n, c.order,
+                                 float(nv_arr) if nv_t is None else 0.0, _ptr(nv_t),
+                                 float(clip), llr.data_ptr(), _stream())
+    _lib.check(rc, "_candidate_llrs_batch")
+    return llr.cpu().numpy() if was_np else llr
+
+
 def llr_from_candidates(clist: CandidateList, noise_var: float, c: Constellation,
                         clip: float = LLR_CLIP) -> np.ndarray:
-    """List max-log LLRs over a candidate list (detect.py:440-462); host-side
-    post-processing of one GPU candidate list for the single-instance API."""
+    """List max-log LLRs over one candidate list (detect.py:455-462)."""
     if clist.n_paths < 1:
         raise ValueError("empty candidate list")
-    bits = bits_from_labels(clist.labels, c).astype(bool)   # (P, N, bps)
-    mm = clist.metrics[:, None, None]
-    min1 = np.where(bits, mm, np.inf).min(axis=0)
-    min0 = np.where(~bits, mm, np.inf).min(axis=0)
-    with np.errstate(invalid="ignore"):
-        llr = (min1 - min0) / noise_var
-    return np.clip(llr, -clip, clip)
+    return _candidate_llrs_batch(np.asarray(clist.labels)[None],
+                                 np.asarray(clist.metrics)[None], noise_var, c, clip)[0]
+
+
+def mpnl_detect_llrs(plan: BatchPathPlan, h, y, c: Constellation, noise_var=None,
+                     clip: float = LLR_CLIP):
+    """The link simulator's MPNL soft output (linksim.py:151-155):
+    `mpnl_detect_batch` then `_candidate_llrs_batch`, with the candidate list
+    kept on the device between the two kernels.  `noise_var` defaults to the
+    plan's.  Returns LLRs shaped like y's leading axes + (N, log2 Q)."""
+    was_np = not isinstance(y, torch.Tensor)
+    yt = y if not was_np else torch.from_numpy(np.ascontiguousarray(np.asarray(y))).to(_device())
+    labels, metrics, _ = mpnl_detect_batch(plan, h, yt, c)
+    lead = labels.shape[:-2]
+    n, p = labels.shape[-1], labels.shape[-2]
+    nv = plan.noise_var if noise_var is None else noise_var
+    if isinstance(nv, np.ndarray) and nv.ndim:
+        nv = nv.reshape(-1)
+    llr = _candidate_llrs_batch(labels.reshape(-1, p, n), metrics.reshape(-1, p), nv, c, clip)
+    llr = llr.reshape(*lead, n, c.bits_per_symbol)
+    return llr.cpu().numpy() if was_np else llr
 
 
 def mpnl_detect(plan: PathPlan, inp: DetectorInput):
