@@ -156,6 +156,66 @@ static __device__ __noinline__ int ex_expanded_symbol(const TreeParams& tp, cons
   return ((bq / L) << 3) | (bq % L);
 }
 
+// The e (<= EM) nearest points of each parent's centre at listed layer pos, in
+// (distance, label) order: thread per parent, one unrolled pass over the Q
+// points with an insertion into a sorted register list.  Centre and distance
+// key are computed exactly as in the rank count of exact_kernel_t (identical
+// expressions), so the lists are identical.
+template <int N, int L, int EM>
+__device__ __noinline__ void ex_scan_lists(const TreeParams& tp, const ExLayout& lo,
+                                           uint8_t* lists, const double2* Rs, const double2* zs,
+                                           int pos, int npar, int e) {
+  constexpr int Q = L * L;
+  constexpr int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
+  for (int par = threadIdx.x; par < npar; par += EX_THREADS) {
+    const int p0 = par * tp.stride[pos + 1];
+    double ur = zs[pos].x, ui = zs[pos].y;
+    for (int j = N - 1; j > pos; --j) {
+      int ir, ii;
+      const int ej = tp.e[j];
+      if (lo.listed[j]) {
+        const uint8_t b = lists[lo.list_off[j] + p0 / tp.stride[j]];
+        ir = b >> 3; ii = b & 7;
+      } else {
+        const int d = (p0 / tp.stride[j]) % ej;
+        ir = d / L; ii = d % L;
+      }
+      const double sr = level_at<L>(ir), si = level_at<L>(ii);
+      const double2 r = Rs[pos * N + j];
+      ur -= r.x * sr - r.y * si;
+      ui -= r.x * si + r.y * sr;
+    }
+    const double rpp = Rs[pos * N + pos].x;
+    const double cr = ur / rpp, ci = ui / rpp;
+    double bd[EM];
+    int bl[EM], bq[EM];
+#pragma unroll
+    for (int k = 0; k < EM; ++k) { bd[k] = CUDART_INF; bl[k] = 1 << 30; bq[k] = 0; }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = q / L, j = q % L;
+      const double dr = cr - level_at<L>(i), di = ci - level_at<L>(j);
+      const double d = dr * dr + di * di;
+      const int lb = (gray_code(i) << h) | gray_code(j);
+      bool lt[EM];
+#pragma unroll
+      for (int k = 0; k < EM; ++k) lt[k] = d < bd[k] || (d == bd[k] && lb < bl[k]);
+#pragma unroll
+      for (int k = EM - 1; k >= 1; --k) {
+        if (lt[k]) {
+          bd[k] = lt[k - 1] ? bd[k - 1] : d;
+          bl[k] = lt[k - 1] ? bl[k - 1] : lb;
+          bq[k] = lt[k - 1] ? bq[k - 1] : q;
+        }
+      }
+      if (lt[0]) { bd[0] = d; bl[0] = lb; bq[0] = q; }
+    }
+#pragma unroll
+    for (int k = 0; k < EM; ++k)
+      if (k < e) lists[lo.list_off[pos] + par * e + k] = (uint8_t)(((bq[k] / L) << 3) | (bq[k] % L));
+  }
+}
+
 template <int N, int L>
 __global__ void __launch_bounds__(EX_THREADS)
 exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
@@ -258,6 +318,15 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
         __syncthreads();
         const int e = tp.e[pos];
         const int npar = P / tp.stride[pos + 1];
+        if (e <= 8 && npar * Q > 2 * EX_THREADS) {
+          // many parents, short lists: thread per parent, one pass over the Q
+          // points keeping the e smallest (distance, label) in registers --
+          // O(Q) per parent instead of the O(Q^2) rank count below (same key)
+          if (e <= 2) ex_scan_lists<N, L, 2>(tp, lo, lists, Rs, zs, pos, npar, e);
+          else if (e <= 4) ex_scan_lists<N, L, 4>(tp, lo, lists, Rs, zs, pos, npar, e);
+          else ex_scan_lists<N, L, 8>(tp, lo, lists, Rs, zs, pos, npar, e);
+          continue;
+        }
         for (int it = tid; it < npar * Q; it += EX_THREADS) {
           const int par = it / Q, q = it % Q;
           const int p0 = par * tp.stride[pos + 1];

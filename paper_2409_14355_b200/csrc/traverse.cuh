@@ -276,6 +276,9 @@ __device__ __forceinline__ void guard_mark(float d, float th, unsigned bit, floa
 // stop after layer `stop` (phase re-traces).
 // SH (NS == 2): the lane's two paths are siblings under the top layer (same
 // top symbol): the top layer's PED term and row updates are computed once.
+#ifndef MPNL_QDESC
+#define MPNL_QDESC 1
+#endif
 template <int N, int L, int NS, bool GUARD, bool LAB, bool SAMEV = false, bool SH = false>
 __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* __restrict__ zs,
                                                const float* __restrict__ thr,
@@ -365,10 +368,17 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
       const u64 e2 = ffma2(pk2(-c2r, -c2r), g2[s], acc[s][pos]);   // c2r n + u
       ped2[s] = ffma2(e2, e2, ped2[s]);
     }
-    // push this layer's symbols into the rows below: acc_k += r''_k,pos * s
+    // push this layer's symbols into the rows below: acc_k += r''_k,pos * s.
+    // Row pairs are walked top-down so the row the next layer slices (pos - 1)
+    // is updated first and the other rows' updates fill its latency.
     const float4* rc = rc4 + pos * NPP;
 #pragma unroll
-    for (int q = 0; q < (pos + 1) / 2; ++q) {
+    for (int qq = 0; qq < (pos + 1) / 2; ++qq) {
+#if MPNL_QDESC
+      const int q = (pos + 1) / 2 - 1 - qq;
+#else
+      const int q = qq;
+#endif
       const float4 r = rc[q];              // {rr_2q, ri_2q, rr_2q+1, ri_2q+1}
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
@@ -672,6 +682,21 @@ __device__ __forceinline__ void select_nearest(float xl, float yl, int E, int th
 // to x, ties to the lower level), K <= L
 template <int L, int K>
 __device__ __forceinline__ void se_order_k(float x, int (&lev)[K], float (&d)[K]) {
+  if constexpr (L == 4) {
+    // 16-QAM axis: the order is fixed by the interval of x among the midpoints
+    // {0.5, 1, 1.5, 2, 2.5} (ties to the lower level): idx = ceil(2x - 1)
+    // clamped to [0, 5], then 2-bit levels from a 6-byte table.  Same distances
+    // as the generic walk; the order can differ only between equidistant
+    // levels, which the selection's cut guard covers (equal keys at the cut).
+    const int idx = min(max(__float2int_ru(fmaf(x, 2.f, -1.f)), 0), 5);
+    const unsigned code = (unsigned)(0x1B1E36C9E1E4ull >> (8 * idx));
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      lev[r] = (int)((code >> (2 * r)) & 3u);
+      d[r] = (x - lev[r]) * (x - lev[r]);
+    }
+    return;
+  }
   const int n0 = (int)rintf(fminf(fmaxf(x, 0.f), (float)(L - 1)));
   int lo = n0 - 1, hi = n0 + 1;
   lev[0] = n0;
@@ -956,7 +981,7 @@ prep2_kernel(const DetectArgs a, const TreeParams tp, int chunks, int pos_sel) {
                                        : rcol_at(tab + tl.off_rcol, NPP, pos_sel, N - 1);
     uint8_t* out = a.lists + gv * tp.list_bytes + tp.list_off[pos_sel];
     const int st = tp.stride[pos_sel + 1];
-#pragma unroll 1
+#pragma unroll 2
     for (int par = j; par < npar; par += TPV) {
       float xr = zsr, xi = zsi;
       if (npar > 1) acc_step(xr, xi, r2.x, r2.y, (float)(par / L), (float)(par % L));
