@@ -106,6 +106,22 @@ int mpnl_detect_hard_host(const void* h, int h_is_f64, const void* y, int y_is_f
                           float* metric, int64_t chunk_channels, void* workspace,
                           int64_t workspace_bytes, void* stream);
 
+/* Device-buffer plan + hard detection of a whole batch (the cli._bench_chunk
+ * call, cli.py:236-239, on device-resident h and y): the channels are split
+ * into `groups` (1..4) contiguous ranges, each planned and detected on its own
+ * internal stream forked from / joined back into `stream`, so one group's
+ * latency-bound stages overlap another's traversal.  Same results as
+ * mpnl_plan + mpnl_detect_hard on the whole batch.  Workspace: device bytes
+ * from mpnl_group_workspace_bytes (plans of all channels + one detection
+ * workspace per group). */
+int64_t mpnl_group_workspace_bytes(int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
+                                   const int64_t* expansions, int groups);
+int mpnl_plan_detect_hard(const void* h, int h_is_f64, const void* y, int y_is_f64,
+                          int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
+                          const int64_t* expansions, double noise_var, uint8_t* hard,
+                          float* metric, int groups, void* workspace,
+                          int64_t workspace_bytes, void* stream);
+
 /* Full candidate list (reference-compatible mpnl_detect_batch), fp64:
  * labels (B, P, n) uint8 in path order and stream order, metrics (B, P)
  * float64, best (B,) int64, B = n_ch * v_per_ch, P = prod(expansions). */

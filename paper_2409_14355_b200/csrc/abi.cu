@@ -642,6 +642,108 @@ extern "C" int mpnl_detect_hard_host(const void* h, int h_is_f64, const void* y,
   return MPNL_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// Device-buffer plan + hard detection of a whole batch in channel groups on forked
+// streams.  Channels are independent, so group g's latency-bound stages (plan, the
+// verify/check of its events, the fp64 fix-up of its few flagged vectors) overlap
+// the other groups' traversal instead of idling the GPU between dependent launches.
+// Results are identical to mpnl_plan + mpnl_detect_hard on the whole batch.
+// ------------------------------------------------------------------------------------------
+namespace {
+#define GROUP_MAX 4
+struct GroupPipe {
+  bool init = false;
+  cudaStream_t gs[GROUP_MAX];
+  cudaEvent_t fork, done[GROUP_MAX];
+};
+thread_local GroupPipe g_grp;
+
+int group_init() {
+  if (g_grp.init) return MPNL_OK;
+  int lo = 0, hi = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);   // hi = greatest priority
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_grp.fork, cudaEventDisableTiming);
+  for (int i = 0; i < GROUP_MAX && e == cudaSuccess; ++i) {
+    // earlier groups first: their short tail kernels take free SM slots ahead
+    // of the next group's traversal CTAs
+    const int pr = std::min(lo, hi + i);
+    e = cudaStreamCreateWithPriority(&g_grp.gs[i], cudaStreamNonBlocking, pr);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_grp.done[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "group streams");
+  g_grp.init = true;
+  return MPNL_OK;
+}
+
+struct GroupLayout {
+  HostPlan plan;
+  int64_t ws0, ws_bytes, total;
+  GroupLayout(int64_t n_ch, int64_t v, int m, int n, int groups, int list_bytes)
+      : plan(n_ch, m, n, 0) {
+    const int64_t cg = (n_ch + groups - 1) / groups;
+    ws_bytes = (Workspace(cg * v, list_bytes, n).total + 255) & ~int64_t(255);
+    ws0 = plan.total;
+    total = ws0 + groups * ws_bytes;
+  }
+};
+}  // namespace
+
+extern "C" int64_t mpnl_group_workspace_bytes(int64_t n_ch, int64_t v_per_ch, int m, int n,
+                                              int q, const int64_t* expansions, int groups) {
+  const int L = levels_for(q);
+  if (!L || n < 1 || n > MPNL_MAX_N || n_ch < 0 || groups < 1 || groups > GROUP_MAX) return -1;
+  TreeBuild tb = build_tree(n, L, expansions);
+  if (!tb.ok) return -1;
+  return GroupLayout(n_ch, v_per_ch, m, n, groups, tb.tp.list_bytes).total;
+}
+
+extern "C" int mpnl_plan_detect_hard(const void* h, int h_is_f64, const void* y, int y_is_f64,
+                                     int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
+                                     const int64_t* expansions, double noise_var, uint8_t* hard,
+                                     float* metric, int groups, void* workspace,
+                                     int64_t workspace_bytes, void* stream) {
+  if (int rc = check_dims(m, n, q)) return rc;
+  if (n_ch < 0 || v_per_ch < 0) return fail(MPNL_EINVAL, "negative batch");
+  if (groups < 1 || groups > GROUP_MAX) return fail(MPNL_EINVAL, "groups must be in 1..4");
+  if (n_ch == 0 || v_per_ch == 0) return MPNL_OK;
+  const int L = levels_for(q);
+  TreeBuild tb = build_tree(n, L, expansions);
+  if (!tb.ok) return fail(MPNL_EINVAL, tb.err);
+  const int G = (int)std::min<int64_t>(groups, n_ch);
+  const GroupLayout gl(n_ch, v_per_ch, m, n, G, tb.tp.list_bytes);
+  if (workspace_bytes < gl.total) return fail(MPNL_EINVAL, "workspace too small");
+  if (int rc = group_init()) return rc;
+  cudaStream_t main = (cudaStream_t)stream;
+  char* pb = reinterpret_cast<char*>(workspace);
+  const int64_t tf = TableLayout(m, n).total;
+  const int hb = h_is_f64 ? 16 : 8, yb = y_is_f64 ? 16 : 8;
+  const int64_t cg = (n_ch + G - 1) / G;
+  cudaError_t e = cudaEventRecord(g_grp.fork, main);
+  for (int g = 0; g < G && e == cudaSuccess; ++g) {
+    const int64_t c0 = g * cg, cn = std::min(cg, n_ch - c0);
+    if (cn <= 0) break;
+    cudaStream_t st = g_grp.gs[g];
+    e = cudaStreamWaitEvent(st, g_grp.fork, 0);
+    if (e != cudaSuccess) break;
+    int32_t* perm = reinterpret_cast<int32_t*>(pb + gl.plan.perm) + c0 * n;
+    double2* r64 = reinterpret_cast<double2*>(pb + gl.plan.r64) + c0 * n * n;
+    double2* qh64 = reinterpret_cast<double2*>(pb + gl.plan.qh64) + c0 * n * m;
+    float* tab = reinterpret_cast<float*>(pb + gl.plan.tables) + c0 * tf;
+    if (int rc = mpnl_plan((const char*)h + c0 * m * n * hb, h_is_f64, cn, m, n, q, noise_var,
+                           perm, r64, qh64, tab, st))
+      return rc;
+    if (int rc = mpnl_detect_hard(perm, r64, qh64, tab, (const char*)y + c0 * v_per_ch * m * yb,
+                                  y_is_f64, cn, v_per_ch, m, n, q, expansions, noise_var,
+                                  hard + c0 * v_per_ch * n, metric + c0 * v_per_ch, nullptr,
+                                  pb + gl.ws0 + g * gl.ws_bytes, gl.ws_bytes, st))
+      return rc;
+    e = cudaEventRecord(g_grp.done[g], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(main, g_grp.done[g], 0);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "group streams");
+  return MPNL_OK;
+}
+
 // ---- FFMA throughput probe (roofline denominator) ----
 __global__ void ffma_probe_kernel(float* out, int iters) {
   float x0 = threadIdx.x * 1e-3f, x1 = x0 + 1.f, x2 = x0 + 2.f, x3 = x0 + 3.f;

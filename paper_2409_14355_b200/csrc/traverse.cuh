@@ -1096,7 +1096,10 @@ __device__ __forceinline__ void trav_issue(const DetectArgs& a, const TravSmem& 
 // VPI = true : vpi = 32 PT / P vectors per item, one batch.
 // SH: (non-VPI, PT = 2) lane l holds the sibling paths 2l, 2l + 1 of a batch
 // (same top symbol: requires an even top-layer stride), sharing the top layer.
-template <int N, int L, bool VPI, bool SH = false>
+// ONEB: (SH, P == 32 PT) every vector is exactly one full batch: the path
+// bookkeeping is compile-time (loop-invariant) and the lane's two paths are
+// ordered with one compare instead of running top-3 inserts.
+template <int N, int L, bool VPI, bool SH = false, bool ONEB = false>
 __global__ void __launch_bounds__(TravCfg<N>::MAXT, TravCfg<N>::MINB)
 traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   constexpr int PT = TravCfg<N>::PT;
@@ -1128,7 +1131,8 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   }
   const int P = tparam.n_paths;
   const int lbytes = tparam.list_bytes;
-  const int bpv = VPI ? 1 : a.bpv;
+  static_assert(!ONEB || (SH && !VPI && TravCfg<N>::PT == 2), "ONEB needs sibling pairs");
+  const int bpv = (VPI || ONEB) ? 1 : a.bpv;
   // paths are fixed per lane when one batch covers them: precompute the
   // expanded layers' symbols (float pair) / list indices once
   u64* xs = reinterpret_cast<u64*>(sm + so.xs) + tid;
@@ -1244,7 +1248,11 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
 #pragma unroll
         for (int t = 0; t < PT; ++t) {
           const int s = SH ? 2 * lane + t : t * 32 + lane;
-          if (!VPI) {
+          if (ONEB) {
+            vl[t] = 0;
+            pp[t] = s;
+            ok[t] = true;
+          } else if (!VPI) {
             vl[t] = 0;
             pp[t] = b * S + s;
             ok[t] = pp[t] < P;
@@ -1261,7 +1269,14 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         traverse_paths<N, L, PT, true, false, !VPI, SH>(T, zs, thr, lch, tp, lbytes, vl, gvl, pp, ped,
                                                     evm, evp, nullptr, nullptr, -1,
                                                     use_xs ? xs : nullptr);
-        if (!VPI) {   // running top-3; the event bound includes this batch's own best
+        if (ONEB) {   // the lane's two paths, ordered (path 2l < 2l + 1)
+          const bool sw = ped[1] < ped[0];
+          run.m1 = sw ? ped[1] : ped[0];
+          run.p1 = (unsigned)(sw ? pp[1] : pp[0]);
+          run.m2 = sw ? ped[0] : ped[1];
+          run.p2 = (unsigned)(sw ? pp[0] : pp[1]);
+          wbest = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
+        } else if (!VPI) {   // running top-3; the event bound includes this batch's own best
 #pragma unroll
           for (int t = 0; t < PT; ++t)
             if (ok[t]) top3_insert(run, ped[t], (unsigned)pp[t]);

@@ -44,8 +44,11 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
     constexpr bool CAN_SH = TravCfg<NN>::PT == 2;
     const bool sh = CAN_SH && a.vpi <= 1 && tp.n_top >= 1 && tp.stride[NN - 1] % 2 == 0 &&
                     tp.n_paths % 2 == 0;
+    const bool oneb = sh && a.bpv == 1 && tp.n_paths == 32 * TravCfg<NN>::PT;
     auto k = a.vpi > 1 ? traverse_kernel<NN, L, true>
-                       : (sh ? traverse_kernel<NN, L, false, CAN_SH> : traverse_kernel<NN, L, false>);
+                       : (oneb ? traverse_kernel<NN, L, false, CAN_SH, CAN_SH>
+                               : (sh ? traverse_kernel<NN, L, false, CAN_SH>
+                                     : traverse_kernel<NN, L, false>));
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (grid == 0) {
       int nb = 0, dev = 0, sms = 148;

@@ -17,6 +17,8 @@ mpnl_detect_hard           hard composition cli.py:236-239,            K3 fp32 t
                            test_acceptance.py:114-117                  K5 fix-up of flags
 mpnl_hard_output           plan + hard composition from HOST arrays    K1-K5, pipelined
                            (the cli._bench_chunk call, cli.py:236-239) host<->device copies
+mpnl_hard_output_device    the same from DEVICE arrays, channel        K1-K5 on forked
+                           groups overlapped                           streams
 mpnl_preprocess            detect.py:391-400                           K1
 mpnl_detect                detect.py:491-506                           K5
 detect("mpnl", ...)        detect.py:563-576                           K1 + K5
@@ -44,7 +46,8 @@ from .core import LLR_CLIP, Constellation, bits_from_labels
 
 __all__ = [
     "allocate_expansions", "BatchPathPlan", "PathPlan", "mpnl_plan_batch",
-    "mpnl_preprocess", "mpnl_detect_batch", "mpnl_detect_hard", "mpnl_hard_output", "mpnl_detect",
+    "mpnl_preprocess", "mpnl_detect_batch", "mpnl_detect_hard", "mpnl_hard_output",
+    "mpnl_hard_output_device", "mpnl_detect",
     "detect", "DetectorInput", "CandidateList", "DetectionOutput",
     "llr_from_candidates", "mpnl_detect_llrs", "DETECTOR_NAMES", "SingularChannelError",
 ]
@@ -328,6 +331,45 @@ def mpnl_hard_output(h, y, noise_var: float, n_paths: int, c: Constellation, *,
                                    _stream())
     _lib.check(rc, "mpnl_hard_output")
     torch.cuda.current_stream().synchronize()
+    return hard, metric
+
+
+_GROUP_WS: dict = {}
+
+
+def mpnl_hard_output_device(h, y, noise_var: float, n_paths: int, c: Constellation, *,
+                            groups: int = 1, out=None):
+    """Plan + hard-output detection of DEVICE-resident h (n_ch, M, N) and
+    y (n_ch, V, M), one C-ABI call (`mpnl_plan_detect_hard`): the channels
+    run as `groups` contiguous groups on forked streams so one group's
+    latency-bound stages overlap another's traversal.  Same results as
+    mpnl_plan_batch + mpnl_detect_hard.  Returns device (hard (n_ch, V, N)
+    uint8, min_metric (n_ch, V) float32), stream-ordered (no sync)."""
+    lib = _lib.load()
+    hd, h64, _ = _to_dev_complex(h, "h")
+    yd, y64, _ = _to_dev_complex(y, "y")
+    if hd.dim() != 3 or yd.dim() != 3 or yd.shape[0] != hd.shape[0] or yd.shape[2] != hd.shape[1]:
+        raise ValueError("inconsistent channel/observation dimensions")
+    n_ch, m, n = hd.shape
+    v = yd.shape[1]
+    ex, _ = allocate_expansions(n, c.order, n_paths, max(0, n - m))
+    if out is None:
+        hard = torch.empty((n_ch, v, n), dtype=torch.uint8, device=yd.device)
+        metric = torch.empty((n_ch, v), dtype=torch.float32, device=yd.device)
+    else:
+        hard, metric = out
+    nb = int(lib.mpnl_group_workspace_bytes(n_ch, v, m, n, c.order, ex.ctypes.data, int(groups)))
+    if nb < 0:
+        raise ValueError("unsupported configuration")
+    ws = _GROUP_WS.get(yd.device)
+    if ws is None or ws.numel() < nb:
+        ws = torch.empty(nb, dtype=torch.uint8, device=yd.device)
+        _GROUP_WS[yd.device] = ws
+    rc = lib.mpnl_plan_detect_hard(hd.data_ptr(), int(h64), yd.data_ptr(), int(y64), n_ch, v, m,
+                                   n, c.order, ex.ctypes.data, float(noise_var), hard.data_ptr(),
+                                   metric.data_ptr(), int(groups), ws.data_ptr(), ws.numel(),
+                                   _stream())
+    _lib.check(rc, "mpnl_hard_output_device")
     return hard, metric
 
 
