@@ -327,7 +327,10 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
             g2[s] = x;
           } else {
             const unsigned b = lists[(SAMEV ? 0 : (int)gvl[s]) * list_bytes + (int)(unsigned)x];
-            g2[s] = pk2(-(float)(b >> 3), -(float)(b & 7u));
+            // -(float)k for k < 8 without I2F: MAGIC - (MAGIC + k), one FADD2
+            g2[s] = fsub2(pk2(MPNL_MAGIC, MPNL_MAGIC),
+                          pk2(__uint_as_float(0x4B400000u | (b >> 3)),
+                              __uint_as_float(0x4B400000u | (b & 7u))));
           }
         }
       } else {
@@ -1182,15 +1185,9 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     const int c = seg / ipc;
     const int ibase = c * ipc, vbase = c * V;
     const int seg_end = min(it_end, ibase + ipc);
-    __syncthreads();   // previous segment's tables no longer in use (and xs / tp ready)
-    {
-      const float4* src = reinterpret_cast<const float4*>(a.tables + (int64_t)c * tl.total);
-      float4* dst = reinterpret_cast<float4*>(tab);
-      for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
-    }
-    __syncthreads();
     // warp w owns the balanced item range [wb, we) of the segment, walked in
-    // chunks of so.ck items (contiguous vectors, one bulk-copy group each)
+    // chunks of so.ck items (contiguous vectors, one bulk-copy group each); the
+    // first chunk's copies are issued before the table staging (they overlap)
     const int wb = seg + (int)((int64_t)warp * (seg_end - seg) / nw);
     const int we = seg + (int)((int64_t)(warp + 1) * (seg_end - seg) / nw);
     const int nchunk = (we - wb + so.ck - 1) / so.ck;
@@ -1202,6 +1199,13 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       trav_issue<N>(a, so, wb0, wbar, vbase + (i0 - ibase) * nvi,
                     min((i1 - ibase) * nvi, V) - (i0 - ibase) * nvi, lbytes);
     }
+    __syncthreads();   // previous segment's tables no longer in use (and xs / tp ready)
+    {
+      const float4* src = reinterpret_cast<const float4*>(a.tables + (int64_t)c * tl.total);
+      float4* dst = reinterpret_cast<float4*>(tab);
+      for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
+    }
+    __syncthreads();
     for (; ch < nchunk; ++ch, k ^= 1) {
       if (ch + 1 < nchunk && lane == 0) {
         const int i0 = wb + (ch + 1) * so.ck;
@@ -1333,9 +1337,18 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       if (!VPI) {
         // b1 = wbest; the 2nd path and the 3rd metric only matter for a near-tie
         const unsigned k1 = __float_as_uint(wbest);
-        const unsigned q1 =
-            __reduce_min_sync(0xffffffffu, __float_as_uint(run.m1) == k1 ? run.p1 : 0xffffffffu);
-        if (__float_as_uint(run.m1) == k1 && run.p1 == q1) top3_pop(run);
+        unsigned q1;
+        if (ONEB) {
+          // lane l holds paths 2l, 2l + 1: the lowest lane holding the best
+          // metric holds the lowest such path (no second reduction on the chain)
+          const int wl = __ffs(__ballot_sync(0xffffffffu, __float_as_uint(run.m1) == k1)) - 1;
+          q1 = __shfl_sync(0xffffffffu, run.p1, wl);
+          if (lane == wl) top3_pop(run);
+        } else {
+          q1 = __reduce_min_sync(0xffffffffu,
+                                 __float_as_uint(run.m1) == k1 ? run.p1 : 0xffffffffu);
+          if (__float_as_uint(run.m1) == k1 && run.p1 == q1) top3_pop(run);
+        }
         const float b2 = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(run.m1)));
         unsigned q2 = 0xffffffffu;
         float b3 = b2;
@@ -1399,10 +1412,20 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
                                                    tl.off_lay)[o];
     }
   }
+  // the CTA's z' rows (contiguous) and its output labels go through shared
+  // memory: coalesced 16-byte loads in, 4-byte stores out
+  // (N <= 16; larger N reads its rows directly: static shared memory limit)
+  constexpr bool STZ = N <= 16;
+  __shared__ float4 zsh[STZ ? 128 * NPP : 1];
+  __shared__ __align__(16) uint8_t osh[128 * N];
+  const int nvb = (int)min((int64_t)blockDim.x, B - g0);
+  if (STZ)
+    for (int i = threadIdx.x; i < nvb * NPP; i += blockDim.x) zsh[i] = a.zq[g0 * NPP + i];
   __syncthreads();
   const int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
   const int64_t gv = g0 + threadIdx.x;
-  if (gv >= B) return;
+  const bool live = gv < B;
+  if (live) {
   const int64_t c = gv / a.V;
   TabPtrs T;
   if (c - c0 < nst) {
@@ -1411,9 +1434,12 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
   } else {
     T = tab_ptrs(a.tables + c * (int64_t)tl.total, m, N);
   }
-  float4 zl[NPP];
+  float4 zreg[STZ ? 1 : NPP];
+  if (!STZ) {
 #pragma unroll
-  for (int q = 0; q < NPP; ++q) zl[q] = a.zq[gv * NPP + q];
+    for (int q = 0; q < (STZ ? 1 : NPP); ++q) zreg[q] = a.zq[gv * NPP + q];
+  }
+  const float4* zl = STZ ? zsh + threadIdx.x * NPP : zreg;
   const uint8_t* vlist = a.lists + gv * tp.list_bytes;
   const float4 res = a.vres[gv];
   const int2 pth = a.vpath[gv];
@@ -1440,13 +1466,24 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
   }
   const float corr = a.metric_offset ? a.vaux[gv].y : 0.f;
   const int32_t* pc = a.perm + c * N;
-  uint8_t* out = a.hard + gv * N;
+  uint8_t* out = osh + threadIdx.x * N;
 #pragma unroll
   for (int pos = 0; pos < N; ++pos) {
     const int ir = lab[pos] >> 3, ii = lab[pos] & 7;
     out[pc[pos]] = (uint8_t)((gray_code(ir) << h) | gray_code(ii));
   }
   a.metric[gv] = res.x + corr;
+  }
+  __syncthreads();
+  uint8_t* dst = a.hard + g0 * N;
+  const int nb = nvb * N;
+  if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+    for (int i = threadIdx.x; i < nb / 4; i += blockDim.x)
+      reinterpret_cast<unsigned*>(dst)[i] = reinterpret_cast<const unsigned*>(osh)[i];
+    for (int i = (nb & ~3) + threadIdx.x; i < nb; i += blockDim.x) dst[i] = osh[i];
+  } else {
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = osh[i];
+  }
 }
 
 // ===========================================================================
