@@ -729,6 +729,52 @@ __device__ __forceinline__ void select_nearest_e(float xl, float yl, unsigned& w
   float dx[KK], dy[KK];
   se_order_k<L, KK>(xl, ox, dx);
   se_order_k<L, KK>(yl, oy, dy);
+  if constexpr ((E == 2 || E == 4) && KK >= 3) {
+    // The merge below, resolved in closed form (same picks, same tie rules,
+    // same kprev / knext values).  R_t = dx0 + dy_t (row 0), C_t = dx_t + dy0
+    // (column 0), D = dx1 + dy1; both runs ascend and D >= R1, C1.
+    auto R = [&](int t) { return t < KK ? dx[0] + dy[t] : INF; };
+    auto C = [&](int t) { return t < KK ? dx[t] + dy[0] : INF; };
+    auto lr = [&](int t) { return ((unsigned)ox[0] << 3) | (unsigned)oy[t < KK ? t : 0]; };
+    auto lcl = [&](int t) { return ((unsigned)ox[t < KK ? t : 0] << 3) | (unsigned)oy[0]; };
+    const float R1 = R(1), C1 = C(1), R2 = R(2), C2 = C(2);
+    word = ((unsigned)ox[0] << 3) | (unsigned)oy[0];
+    if constexpr (E == 2) {
+      const bool ta = R1 <= C1;
+      word |= (ta ? lr(1) : lcl(1)) << 8;
+      kprev = ta ? R1 : C1;
+      knext = ta ? fminf(R2, C1) : fminf(R1, C2);
+    } else {
+      const float R3 = R(3), C3 = C(3), D = dx[1] + dy[1];
+      const unsigned ld = ((unsigned)ox[1] << 3) | (unsigned)oy[1];
+      const bool rr = R2 <= C1;               // picks R1, R2, then R3 | C1
+      const bool cc = !rr && C2 < R1;         // picks C1, C2, then C3 | R1
+      const bool t3r = R3 <= C1, t3c = R1 <= C3;
+      const bool a3 = R2 <= C2 && R2 <= D, b3 = !a3 && C2 <= D;   // mid: R1, C1, then
+      unsigned b1, b2, b3l;
+      float k3, k4;
+      if (rr) {
+        b1 = lr(1); b2 = lr(2);
+        b3l = t3r ? lr(3) : lcl(1);
+        k3 = t3r ? R3 : C1;
+        k4 = t3r ? fminf(R(4), C1) : fminf(fminf(R3, C2), D);
+      } else if (cc) {
+        b1 = lcl(1); b2 = lcl(2);
+        b3l = t3c ? lr(1) : lcl(3);
+        k3 = t3c ? R1 : C3;
+        k4 = t3c ? fminf(fminf(R2, C3), D) : fminf(R1, C(4));
+      } else {
+        b1 = lr(1); b2 = lcl(1);
+        b3l = a3 ? lr(2) : (b3 ? lcl(2) : ld);
+        k3 = a3 ? R2 : (b3 ? C2 : D);
+        k4 = a3 ? fminf(fminf(R3, C2), D) : (b3 ? fminf(fminf(R2, C3), D) : fminf(R2, C2));
+      }
+      word |= (b1 << 8) | (b2 << 16) | (b3l << 24);
+      kprev = k3;
+      knext = k4;
+    }
+    return;
+  }
   float ra[K], cb[K];
   unsigned la[K], lb[K];
 #pragma unroll
