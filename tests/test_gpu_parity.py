@@ -219,3 +219,25 @@ def test_large_batch_tiled_golden(name):
         _check_hard(hard[r].astype(np.int64), metric[r].astype(np.float64), g["hard"], g["m1"],
                     g["m2"], f"{name} tile {r}")
     assert (hard == hard[:1]).all() and (metric == metric[:1]).all()
+
+
+@pytest.mark.parametrize("name,n_rb", [("C2", 9), ("C3", 5), ("C5P16", 3)])
+def test_device_one_call_matches_staged_path(name, n_rb):
+    """mpnl_plan_detect_hard (one C-ABI call, 1..4 channel groups on forked
+    streams) is identical to mpnl_plan_batch + mpnl_detect_hard."""
+    import torch
+    det = _det()
+    d = generate(name, n_rb=n_rb)
+    cfg = d["cfg"]
+    c = constellation_for(cfg.order)
+    h = torch.from_numpy(d["h"]).cuda()
+    y = torch.from_numpy(d["y"]).cuda()
+    nv = float(d["nv"][0])
+    plan = det.mpnl_plan_batch(h, nv, cfg.n_paths, c)
+    ref_h, ref_m = det.mpnl_detect_hard(plan, h, y, c)
+    for g in (1, 2, 3, 4):
+        hd, md = det.mpnl_hard_output_device(h, y, nv, cfg.n_paths, c, groups=g)
+        torch.cuda.synchronize()
+        assert torch.equal(hd, ref_h) and torch.equal(md, ref_m), f"groups={g}"
+    with pytest.raises(ValueError):
+        det.mpnl_hard_output_device(h, y, nv, cfg.n_paths, c, groups=5)
