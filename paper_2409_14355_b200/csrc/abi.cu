@@ -600,12 +600,27 @@ extern "C" int mpnl_detect_hard_host(const void* h, int h_is_f64, const void* y,
   e = cudaEventRecord(g_pipe.planned, comp);
   for (int i = 0; i < HOST_SLOTS && e == cudaSuccess; ++i)
     e = cudaStreamWaitEvent(g_pipe.cs[i], g_pipe.planned, 0);
-  const int64_t K = (n_ch + C - 1) / C;
+  // chunk schedule: tapered ends (a quarter chunk first and last) when the batch
+  // spans more than two chunks, so the kernels start after a short first upload
+  // and the un-overlapped tail (last chunk's kernels + download) stays short
+  std::vector<int64_t> starts;
+  {
+    const int64_t taper = std::max<int64_t>(1, C / 4);
+    const bool tap = n_ch > 2 * C;
+    int64_t pos = 0;
+    if (tap) { starts.push_back(0); pos = taper; }
+    while (pos < n_ch) {
+      starts.push_back(pos);
+      const int64_t rem = n_ch - pos;
+      pos += (tap && rem > taper && rem <= C + taper) ? rem - taper : std::min(C, rem);
+    }
+  }
+  const int64_t K = (int64_t)starts.size();
   for (int64_t k = 0; k < K && e == cudaSuccess; ++k) {
     const int sl = (int)(k % HOST_SLOTS);
     cudaStream_t cst = g_pipe.cs[sl];   // one compute stream per slot: chunk tails overlap
     char* sb = base + sl * hs.total;
-    const int64_t c0 = k * C, cn = std::min(C, n_ch - c0);
+    const int64_t c0 = starts[k], cn = (k + 1 < K ? starts[k + 1] : n_ch) - c0;
     // upload (slot free once the compute of its previous chunk is done)
     if (k >= HOST_SLOTS) e = cudaStreamWaitEvent(up, g_pipe.done[sl], 0);
     if (e == cudaSuccess)
