@@ -14,25 +14,20 @@ namespace mpnl {
 __device__ __forceinline__ double level_value(int i, int L, double nrm) {
   (void)nrm;
   constexpr double n2 = 1.4142135623730951, n4 = 3.1622776601683795, n8 = 6.48074069840786;
-  if (L == 2) return i == 0 ? 1.0 / n2 : -1.0 / n2;
-  if (L == 4) {
-    switch (i) {
-      case 0: return 3.0 / n4;
-      case 1: return 1.0 / n4;
-      case 2: return -1.0 / n4;
-      default: return -3.0 / n4;
-    }
+  // branch-free (a switch compiles to an indirect jump, and the lanes of a warp
+  // index different levels): |lv| from the mirrored index, then the sign --
+  // the same compile-time quotients, negation is exact
+  const bool neg = 2 * i >= L;
+  const int k = neg ? L - 1 - i : i;
+  double v;
+  if (L == 2) {
+    v = 1.0 / n2;
+  } else if (L == 4) {
+    v = k == 0 ? 3.0 / n4 : 1.0 / n4;
+  } else {
+    v = k == 0 ? 7.0 / n8 : (k == 1 ? 5.0 / n8 : (k == 2 ? 3.0 / n8 : 1.0 / n8));
   }
-  switch (i) {
-    case 0: return 7.0 / n8;
-    case 1: return 5.0 / n8;
-    case 2: return 3.0 / n8;
-    case 3: return 1.0 / n8;
-    case 4: return -1.0 / n8;
-    case 5: return -3.0 / n8;
-    case 6: return -5.0 / n8;
-    default: return -7.0 / n8;
-  }
+  return neg ? -v : v;
 }
 
 static __device__ __noinline__ int nearest_level_f64(double c, int L, double nrm) {
