@@ -30,6 +30,26 @@ __device__ __forceinline__ double level_value(int i, int L, double nrm) {
   return neg ? -v : v;
 }
 
+// level_value for a RUN-TIME index (lanes holding different levels): the same
+// constants chosen with predicated selects that ptxas cannot turn back into an
+// indirect jump.  (level_value stays foldable for compile-time indices.)
+__device__ __forceinline__ double selp_d(double a, double b, bool p) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(r) : "d"(a), "d"(b), "r"((unsigned)p));
+  return r;
+}
+__device__ __forceinline__ double level_value_rt(int i, int L) {
+  constexpr double n2 = 1.4142135623730951, n4 = 3.1622776601683795, n8 = 6.48074069840786;
+  const bool neg = 2 * i >= L;
+  const int k = neg ? L - 1 - i : i;
+  double v;
+  if (L == 2) v = 1.0 / n2;
+  else if (L == 4) v = selp_d(3.0 / n4, 1.0 / n4, k == 0);
+  else v = selp_d(7.0 / n8, selp_d(5.0 / n8, selp_d(3.0 / n8, 1.0 / n8, k == 2), k == 1), k == 0);
+  return selp_d(-v, v, neg);
+}
+
 static __device__ __noinline__ int nearest_level_f64(double c, int L, double nrm) {
   double bd = 1e300;
   int bg = 1 << 30, bi = 0;

@@ -1637,7 +1637,7 @@ __device__ __forceinline__ void warp_centre_f64(const DetectArgs& a, int64_t c, 
   double sr_ = 0.0, si_ = 0.0;
   const int j = pos + 1 + lane;
   if (j < n) {
-    const double sr = level_value(labw[j] >> 3, L, nrm), si = level_value(labw[j] & 7, L, nrm);
+    const double sr = level_value_rt(labw[j] >> 3, L), si = level_value_rt(labw[j] & 7, L);
     const double rr = R[2 * j], ri = R[2 * j + 1];
     sr_ = rr * sr - ri * si;
     si_ = rr * si + ri * sr;
@@ -1660,7 +1660,7 @@ __device__ __forceinline__ double warp_ped_f64(const DetectArgs& a, int64_t c, i
     const double2* R = a.r64 + (c * n + lane) * (int64_t)n;
 #pragma unroll 4
     for (int j = lane; j < n; ++j) {
-      const double sr = level_value(labw[j] >> 3, L, nrm), si = level_value(labw[j] & 7, L, nrm);
+      const double sr = level_value_rt(labw[j] >> 3, L), si = level_value_rt(labw[j] & 7, L);
       const double2 r = R[j];
       zr -= r.x * sr - r.y * si;
       zi -= r.x * si + r.y * sr;
@@ -1685,7 +1685,7 @@ __device__ __forceinline__ double warp_sic_f64(const DetectArgs& a, int64_t c, i
     const int j0 = lane > pos ? lane : pos + 1;
 #pragma unroll 4
     for (int j = j0; j < n; ++j) {
-      const double sr = level_value(labw[j] >> 3, L, nrm), si = level_value(labw[j] & 7, L, nrm);
+      const double sr = level_value_rt(labw[j] >> 3, L), si = level_value_rt(labw[j] & 7, L);
       const double2 r = R[lane * n + j];
       zr -= r.x * sr - r.y * si;
       zi -= r.x * si + r.y * sr;
@@ -1703,7 +1703,7 @@ __device__ __forceinline__ double warp_sic_f64(const DetectArgs& a, int64_t c, i
       ir = __shfl_sync(0xffffffffu, lr, q);
       ii = __shfl_sync(0xffffffffu, li, q);
     }
-    const double sr = level_value(ir, L, nrm), si = level_value(ii, L, nrm);
+    const double sr = level_value_rt(ir, L), si = level_value_rt(ii, L);
     if (lane <= q) {
       const double2 r = R[lane * n + q];
       zr -= r.x * sr - r.y * si;
