@@ -14,7 +14,9 @@
 // mpnl_detect_full outputs as they sit in HBM.  The kernel is HBM-bound byte
 // work: one warp per vector, lane = stream, so every path is one coalesced
 // N-byte row read plus a broadcast metric; the 2·bps running minima live in
-// registers.  Grid: persistent warps strided over vectors.
+// registers.  A warp takes G = 32 / N vectors at once (lane = (vector, stream)),
+// so short vectors do not idle most of the warp.  Grid: persistent warps
+// strided over vector groups.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -28,14 +30,18 @@ __global__ void __launch_bounds__(256) candidate_llr_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const bool active = lane < n;
+  const int G = 32 / n;                        // vectors per warp pass
+  const int gi = lane / n, ln = lane - gi * n;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  for (int64_t b = warp; b < B; b += n_warps) {
+  for (int64_t b0 = warp * G; b0 < B; b0 += n_warps * G) {
+    const int64_t b = b0 + gi;
+    const bool active = gi < G && b < B;
+    const int64_t bb = active ? b : b0;        // inactive lanes read a valid row
     double mn1[BPS], mn0[BPS];
 #pragma unroll
     for (int j = 0; j < BPS; ++j) mn1[j] = mn0[j] = inf;
-    const uint8_t* lab = labels + b * P * n + lane;
-    const double* met = metrics + b * P;
+    const uint8_t* lab = labels + bb * P * n + ln;
+    const double* met = metrics + bb * P;
     int64_t p = 0;
     for (; p + 4 <= P; p += 4) {
       unsigned l4[4];
@@ -67,7 +73,7 @@ __global__ void __launch_bounds__(256) candidate_llr_kernel(
     }
     if (active) {
       const double v = nv_vec ? nv_vec[b] : nv;
-      double* out = llr + (b * n + lane) * BPS;
+      double* out = llr + (b * n + ln) * BPS;
 #pragma unroll
       for (int j = 0; j < BPS; ++j) {
         double x = __ddiv_rn(__dsub_rn(mn1[j], mn0[j]), v);
@@ -84,7 +90,7 @@ cudaError_t launch_candidate_llrs(const uint8_t* labels, const double* metrics, 
                                   int64_t P, int n, int bps, double nv, const double* nv_vec,
                                   double clip, double* llr, cudaStream_t st) {
   const int threads = 256;
-  const int64_t warps_needed = B;
+  const int64_t warps_needed = (B + 32 / n - 1) / (32 / n);
   int64_t blocks = (warps_needed + (threads / 32) - 1) / (threads / 32);
   const int64_t cap = 148 * 8;  // 8 resident 256-thread CTAs per SM
   if (blocks > cap) blocks = cap;
