@@ -15,6 +15,7 @@
  *                              and test_acceptance.py:114-117)
  *   mpnl_detect_full       <- mpnl_detect_batch      detect.py:473-488
  *   mpnl_candidate_llrs    <- _candidate_llrs_batch  detect.py:439-453
+ *   mpnl_linear_detect     <- linear_detect_batch    detect.py:528-557
  * INTEGRATION.md shows the ctypes binding a maintainer adds to detect.py.
  */
 #ifndef MPNL_B200_H
@@ -144,6 +145,20 @@ int mpnl_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t n_
                         int64_t n_paths, int n, int q, double noise_var,
                         const double* noise_var_per_vector, double clip, double* llr_out,
                         void* stream);
+
+/* Batched linear ZF (mode 0) / MMSE (mode 1) detection with max-log LLRs
+ * (replaces linear_detect_batch, detect.py:528-557).  Device pointers:
+ * h (B,M,N) and y (B,M) complex128 (interleaved re/im), noise_var scalar or
+ * per vector (noise_var_per_vector, B doubles, or NULL).  Outputs: labels
+ * uint8 (B,N) nearest points, llr float64 (B,N,log2 Q) clipped to +-clip,
+ * optional est complex128 (B,N) equalised symbols (NULL skips), optional
+ * device int32 *n_singular += vectors whose A had a Cholesky pivot below 64 ulp
+ * of its diagonal entry, i.e. singular to working precision (the reference's np.linalg.inv raises LinAlgError there).
+ * Errors: unknown mode -> MPNL_EINVAL; N > 16 or Q not in {4,16,64} -> MPNL_EUNSUPPORTED. */
+int mpnl_linear_detect(const void* h, const void* y, int64_t n_vectors, int m, int n, int q,
+                       int mode, double noise_var, const double* noise_var_per_vector,
+                       double clip, uint8_t* labels_out, double* llr_out, void* est_out,
+                       int32_t* n_singular, void* stream);
 
 /* Scale of the fp32 error bound used by the traversal guard (default 1 =
  * the rigorous bound; <= 0 restores the default).  Diagnostics only. */

@@ -272,3 +272,49 @@ def candidate_llrs(labels, metrics, noise_var, order, clip=20.0):
     with np.errstate(invalid="ignore"):
         llr = (min1 - min0) / nv
     return np.clip(llr, -clip, clip)
+
+
+def _points(order):
+    """Unit-energy Gray QAM points indexed by label (core.py:56-76)."""
+    half = (int(order).bit_length() - 1) // 2
+    n = 1 << half
+    lv = np.empty(n)
+    for pos in range(n):
+        lv[pos ^ (pos >> 1)] = n - 1 - 2 * pos
+    lab = np.arange(order)
+    return (lv[lab >> half] + 1j * lv[lab & (n - 1)]) / np.sqrt(2.0 * (4 ** half - 1) / 3.0)
+
+
+def linear_detect(h, y, noise_var, order, mode, clip=20.0):
+    """Batched ZF / MMSE (detect.py:528-557) with the max-log demapper
+    (core.py:191-206): h (B,M,N), y (B,M) -> (labels (B,N), llrs (B,N,bps),
+    est (B,N)).  np.linalg.inv raises LinAlgError on a singular A, as there."""
+    b, m, n = h.shape
+    hh = h.conj().transpose(0, 2, 1)
+    gram = hh @ h
+    hy = np.einsum("bnm,bm->bn", hh, y)
+    nv = np.broadcast_to(np.asarray(noise_var, dtype=float), (b,))
+    if mode == "zf":
+        a = gram
+    elif mode == "mmse":
+        a = gram + nv[:, None, None] * np.eye(n)
+    else:
+        raise ValueError(f"unknown linear mode {mode!r}")
+    a_inv = np.linalg.inv(a)
+    soft = np.einsum("bij,bj->bi", a_inv, hy)
+    diag = np.real(np.einsum("bii->bi", a_inv))
+    if mode == "zf":
+        est, nv_eff = soft, nv[:, None] * diag
+    else:
+        beta = np.clip(1.0 - nv[:, None] * diag, 1e-12, None)
+        est = soft / beta
+        nv_eff = np.clip((1.0 - beta) / beta, 1e-15, None)
+    pts = _points(order)
+    bps = int(order).bit_length() - 1
+    d = np.abs(est[..., None] - pts) ** 2                          # (B,N,Q)
+    labels = np.argmin(d, axis=-1)
+    bits = ((np.arange(order)[:, None] >> np.arange(bps - 1, -1, -1)) & 1).astype(bool)
+    d1 = np.where(bits.T, d[..., None, :], np.inf).min(axis=-1)    # (B,N,bps)
+    d0 = np.where(~bits.T, d[..., None, :], np.inf).min(axis=-1)
+    llrs = (d1 - d0) / nv_eff[..., None]
+    return labels, np.clip(llrs, -clip, clip), est

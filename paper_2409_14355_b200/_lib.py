@@ -41,6 +41,8 @@ _SIGS = {
                                _vp, _vp, _i32, _vp, _i64, _vp], _i32),
     "mpnl_candidate_llrs": ([_vp, _vp, _i64, _i64, _i32, _i32, _f64, _vp, _f64, _vp, _vp],
                             _i32),
+    "mpnl_linear_detect": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _f64, _vp, _f64, _vp, _vp,
+                            _vp, _vp, _vp], _i32),
     "mpnl_set_guard_scale": ([_f64], None),
     "mpnl_set_stats": ([_vp], None),
     "mpnl_ffma_probe": ([_vp, _i32, _i32, _i32, _vp], _i64),

@@ -33,6 +33,11 @@ MPNL_DECL_PART(8, 0) MPNL_DECL_PART(8, 1) MPNL_DECL_PART(8, 2) MPNL_DECL_PART(8,
 
 namespace mpnl {
 cudaError_t launch_exact(const ExactArgs& a, const TreeParams& tp, int grid, cudaStream_t st);
+cudaError_t launch_linear_detect(const void* h, const void* y, int64_t n_vectors, int m, int n,
+                                 int half_bits, int mmse, double nv_scalar, const double* nv_vec,
+                                 double clip, uint8_t* labels_out, double* llr_out,
+                                 void* est_out, int32_t* n_singular, cudaStream_t stream);
+int linear_max_n();
 cudaError_t launch_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t B,
                                   int64_t P, int n, int bps, double nv, const double* nv_vec,
                                   double clip, double* llr, cudaStream_t st);
@@ -475,6 +480,24 @@ int mpnl_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t n_
                                         noise_var_per_vector, clip, llr_out,
                                         (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "candidate llr kernel");
+  return MPNL_OK;
+}
+
+int mpnl_linear_detect(const void* h, const void* y, int64_t n_vectors, int m, int n, int q,
+                       int mode, double noise_var, const double* noise_var_per_vector,
+                       double clip, uint8_t* labels_out, double* llr_out, void* est_out,
+                       int32_t* n_singular, void* stream) {
+  if (mode != 0 && mode != 1)
+    return fail(MPNL_EINVAL, "unknown linear mode " + std::to_string(mode));
+  if (n < 1 || m < 1 || n_vectors < 0) return fail(MPNL_EINVAL, "inconsistent h/y dimensions");
+  if (n > linear_max_n()) return fail(MPNL_EUNSUPPORTED, "N > 16 streams is not supported");
+  const int L = levels_for(q);
+  if (!L) return fail(MPNL_EUNSUPPORTED, "unsupported constellation order " + std::to_string(q));
+  const int half = q == 4 ? 1 : (q == 16 ? 2 : 3);
+  cudaError_t e = launch_linear_detect(h, y, n_vectors, m, n, half, mode, noise_var,
+                                       noise_var_per_vector, clip, labels_out, llr_out, est_out,
+                                       n_singular, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "linear detect kernel");
   return MPNL_OK;
 }
 

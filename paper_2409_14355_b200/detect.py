@@ -50,6 +50,7 @@ __all__ = [
     "mpnl_hard_output_device", "mpnl_detect",
     "detect", "DetectorInput", "CandidateList", "DetectionOutput",
     "llr_from_candidates", "mpnl_detect_llrs", "DETECTOR_NAMES", "SingularChannelError",
+    "linear_detect_batch",
 ]
 
 
@@ -404,6 +405,55 @@ def mpnl_detect_batch(plan: BatchPathPlan, h, y, c: Constellation):
         outs = [outs[0].cpu().numpy().astype(np.int64), outs[1].cpu().numpy(),
                 outs[2].cpu().numpy()]
     return tuple(outs)
+
+
+# ---------------------------------------------------------------------------
+# linear ZF / MMSE batch detector
+# ---------------------------------------------------------------------------
+
+_LINEAR_MODES = {"zf": 0, "mmse": 1}
+
+
+def linear_detect_batch(h, y, noise_var, c: Constellation, mode: str, *, return_est=False):
+    """Batched ZF / MMSE detection (detect.py:528-557) on the GPU.
+
+    h (B, M, N), y (B, M) numpy or CUDA tensors; noise_var scalar or (B,).
+    Returns (hard labels (B, N) int64, llrs (B, N, log2 Q) float64) as numpy
+    for numpy inputs (device tensors — labels uint8 — for CUDA inputs), plus
+    the equalised symbols (B, N) when return_est.  Same errors as the
+    reference: unknown mode -> ValueError, singular A -> np.linalg.LinAlgError.
+    Soft values and LLRs agree with the reference to fp64 rounding (Cholesky
+    here, LAPACK inverse there); tests pin the tolerance."""
+    if mode not in _LINEAR_MODES:
+        raise ValueError(f"unknown linear mode {mode!r}")
+    lib = _lib.load()
+    ht, _, was_np = _to_dev_complex(h, "h")
+    yt, _, _ = _to_dev_complex(y, "y")
+    ht, yt = ht.to(torch.complex128).contiguous(), yt.to(torch.complex128).contiguous()
+    if ht.dim() != 3 or yt.shape != ht.shape[:2]:
+        raise ValueError("h must be (B, M, N) and y (B, M)")
+    b, m, n = ht.shape
+    dev = ht.device
+    nv_arr = np.asarray(noise_var.cpu() if isinstance(noise_var, torch.Tensor) else noise_var,
+                        dtype=np.float64)
+    nv_t = None
+    if nv_arr.ndim:
+        nv_t = torch.from_numpy(np.broadcast_to(nv_arr, (b,)).copy()).to(dev)
+    labels = torch.empty((b, n), dtype=torch.uint8, device=dev)
+    llr = torch.empty((b, n, c.bits_per_symbol), dtype=torch.float64, device=dev)
+    est = torch.empty((b, n), dtype=torch.complex128, device=dev) if return_est else None
+    n_sing = torch.zeros(1, dtype=torch.int32, device=dev)
+    rc = lib.mpnl_linear_detect(ht.data_ptr(), yt.data_ptr(), b, m, n, c.order,
+                                _LINEAR_MODES[mode], float(nv_arr) if nv_t is None else 0.0,
+                                _ptr(nv_t), float(LLR_CLIP), labels.data_ptr(), llr.data_ptr(),
+                                _ptr(est), n_sing.data_ptr(), _stream())
+    _lib.check(rc, "linear_detect_batch")
+    if int(n_sing.item()):
+        raise np.linalg.LinAlgError("Singular matrix")
+    if was_np:
+        out = (labels.cpu().numpy().astype(np.int64), llr.cpu().numpy())
+        return out + (est.cpu().numpy(),) if return_est else out
+    return (labels, llr, est) if return_est else (labels, llr)
 
 
 # ---------------------------------------------------------------------------
