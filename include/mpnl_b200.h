@@ -151,7 +151,8 @@ int mpnl_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t n_
  * h (B,M,N) and y (B,M) complex128 (interleaved re/im), noise_var scalar or
  * per vector (noise_var_per_vector, B doubles, or NULL).  Outputs: labels
  * uint8 (B,N) nearest points, llr float64 (B,N,log2 Q) clipped to +-clip,
- * optional est complex128 (B,N) equalised symbols (NULL skips), optional
+ * optional est complex128 (B,N) raw equalised symbols A^-1 H^H y (the biased
+ * MMSE output, detect.py:129-136; NULL skips), optional
  * device int32 *n_singular += vectors whose A had a Cholesky pivot below 64 ulp
  * of its diagonal entry, i.e. singular to working precision (the reference's np.linalg.inv raises LinAlgError there).
  * Errors: unknown mode -> MPNL_EINVAL; N > 16 or Q not in {4,16,64} -> MPNL_EUNSUPPORTED. */

@@ -288,7 +288,7 @@ def _points(order):
 def linear_detect(h, y, noise_var, order, mode, clip=20.0):
     """Batched ZF / MMSE (detect.py:528-557) with the max-log demapper
     (core.py:191-206): h (B,M,N), y (B,M) -> (labels (B,N), llrs (B,N,bps),
-    est (B,N)).  np.linalg.inv raises LinAlgError on a singular A, as there."""
+    raw soft A^-1 H^H y (B,N)).  np.linalg.inv raises LinAlgError on a singular A, as there."""
     b, m, n = h.shape
     hh = h.conj().transpose(0, 2, 1)
     gram = hh @ h
@@ -317,4 +317,4 @@ def linear_detect(h, y, noise_var, order, mode, clip=20.0):
     d1 = np.where(bits.T, d[..., None, :], np.inf).min(axis=-1)    # (B,N,bps)
     d0 = np.where(~bits.T, d[..., None, :], np.inf).min(axis=-1)
     llrs = (d1 - d0) / nv_eff[..., None]
-    return labels, np.clip(llrs, -clip, clip), est
+    return labels, np.clip(llrs, -clip, clip), soft

@@ -155,7 +155,7 @@ linear_detect_kernel(const double2* __restrict__ h, const double2* __restrict__ 
       er = x[i].re; ei = x[i].im;
       nv_eff = nv * dg;
     }
-    if (est_out) est_out[v * n + i] = make_double2(er, ei);
+    if (est_out) est_out[v * n + i] = make_double2(x[i].re, x[i].im);   // raw (biased) soft
     // nearest point (first minimum) and max-log bit metrics over all Q points
     double d0[6], d1[6];
     for (int b = 0; b < bps; ++b) { d0[b] = INFINITY; d1[b] = INFINITY; }

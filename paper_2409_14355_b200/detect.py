@@ -50,7 +50,7 @@ __all__ = [
     "mpnl_hard_output_device", "mpnl_detect",
     "detect", "DetectorInput", "CandidateList", "DetectionOutput",
     "llr_from_candidates", "mpnl_detect_llrs", "DETECTOR_NAMES", "SingularChannelError",
-    "linear_detect_batch",
+    "linear_detect_batch", "zf_detect", "mmse_detect",
 ]
 
 
@@ -420,7 +420,8 @@ def linear_detect_batch(h, y, noise_var, c: Constellation, mode: str, *, return_
     h (B, M, N), y (B, M) numpy or CUDA tensors; noise_var scalar or (B,).
     Returns (hard labels (B, N) int64, llrs (B, N, log2 Q) float64) as numpy
     for numpy inputs (device tensors — labels uint8 — for CUDA inputs), plus
-    the equalised symbols (B, N) when return_est.  Same errors as the
+    the raw equalised symbols A^-1 H^H y (B, N) — the biased MMSE output, as
+    the reference's single-instance `soft` — when return_est.  Same errors as the
     reference: unknown mode -> ValueError, singular A -> np.linalg.LinAlgError.
     Soft values and LLRs agree with the reference to fp64 rounding (Cholesky
     here, LAPACK inverse there); tests pin the tolerance."""
@@ -454,6 +455,39 @@ def linear_detect_batch(h, y, noise_var, c: Constellation, mode: str, *, return_
         out = (labels.cpu().numpy().astype(np.int64), llr.cpu().numpy())
         return out + (est.cpu().numpy(),) if return_est else out
     return (labels, llr, est) if return_est else (labels, llr)
+
+
+def zf_detect(inp: "DetectorInput") -> "DetectionOutput":
+    """Zero-forcing, single instance (detect.py:100-119) through the batch
+    kernel (B = 1).  Same SingularChannelError cases: M < N, singular Gram
+    matrix, condition number above 1e12."""
+    if inp.m < inp.n:
+        raise SingularChannelError("ZF requires M >= N")
+    h = np.asarray(inp.h, dtype=complex)
+    if not np.isfinite(c := np.linalg.cond(h)) or c * c > 1e12:   # cond(H^H H) = cond(H)^2
+        raise SingularChannelError("rank-deficient channel")
+    return _linear_single(inp, "zf")
+
+
+def mmse_detect(inp: "DetectorInput") -> "DetectionOutput":
+    """MMSE, single instance (detect.py:122-145) through the batch kernel:
+    `soft` is the raw (biased) MMSE output, slicing and LLRs use the unbiased
+    estimate with the effective noise variance."""
+    return _linear_single(inp, "mmse")
+
+
+def _linear_single(inp, mode):
+    c = inp.constellation
+    try:
+        lab, llr, soft = linear_detect_batch(np.asarray(inp.h)[None], np.asarray(inp.y)[None],
+                                             float(inp.noise_var), c, mode, return_est=True)
+    except np.linalg.LinAlgError:
+        raise SingularChannelError("rank-deficient channel") from None
+    labels = lab[0]
+    hard = c.points[labels]
+    return DetectionOutput(hard=hard, hard_labels=labels, llrs=llr[0],
+                           min_metric=_residual_metric(np.asarray(inp.h), np.asarray(inp.y), hard),
+                           soft=soft[0])
 
 
 # ---------------------------------------------------------------------------
@@ -594,15 +628,20 @@ def mpnl_detect(plan: PathPlan, inp: DetectorInput):
     return clist, out
 
 
-DETECTOR_NAMES = ("mpnl",)
+DETECTOR_NAMES = ("zf", "mmse", "mpnl")
 
 
 def detect(name: str, inp: DetectorInput, n_paths: int = 32) -> DetectionOutput:
     """Name dispatch (detect.py:563-576).  Only the MPNL path is in scope for
-    this library; the reference's zf/mmse/ml/sphere stay in the reference."""
+    this library, plus the linear ZF / MMSE detectors; the
+    reference's ml / sphere stay in the reference."""
     if name == "mpnl":
         plan = mpnl_preprocess(inp.h, inp.noise_var, n_paths, inp.constellation)
         return mpnl_detect(plan, inp)[1]
-    if name in ("zf", "mmse", "ml", "sphere"):
+    if name == "zf":
+        return zf_detect(inp)
+    if name == "mmse":
+        return mmse_detect(inp)
+    if name in ("ml", "sphere"):
         raise NotImplementedError(f"detector {name!r} is outside the MPNL hot path")
     raise ValueError(f"unknown detector {name!r}")

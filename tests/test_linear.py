@@ -95,8 +95,7 @@ def test_gpu_linear_reference_properties():
     np.testing.assert_array_equal(lab, [[0, 3]] * 3)
     for nv in (0.01, 0.5, 2.0):
         _, _, est = D.linear_detect_batch(h, y, nv, q4, "mmse", return_est=True)
-        # soft / beta with beta = 1 - nv / (1 + nv) = 1 / (1 + nv): est = y
-        np.testing.assert_allclose(est, y, rtol=1e-12)
+        np.testing.assert_allclose(est, y / (1 + nv), rtol=1e-12)   # raw (biased) MMSE
     # noiseless consistency and the MMSE -> ZF limit
     rng = np.random.default_rng(5)
     h, _, x = _rand(rng, 256, 6, 4, 16, 0.0)
@@ -126,3 +125,38 @@ def test_gpu_linear_device_tensors():
     olab, ollr, _ = orc.linear_detect(h, y, 0.02, 64, "mmse")
     np.testing.assert_array_equal(lab.cpu().numpy(), olab)
     np.testing.assert_allclose(llr.cpu().numpy(), ollr, rtol=0, atol=LLR_ATOL)
+
+
+@pytest.mark.gpu
+def test_gpu_single_instance_zf_mmse():
+    """zf_detect / mmse_detect / detect("zf"|"mmse") (detect.py:100-145, 563-576)
+    restated from test_detect.py:28-86 on the single-instance shims."""
+    from paper_2409_14355_b200 import detect as D
+    from paper_2409_14355_b200.core import constellation_for
+    q4, q16 = constellation_for(4), constellation_for(16)
+    inp = D.DetectorInput(h=np.eye(2, dtype=complex), y=np.array([q4.points[0], q4.points[3]]),
+                          noise_var=0.1, constellation=q4)
+    np.testing.assert_array_equal(D.zf_detect(inp).hard_labels, [0, 3])
+    np.testing.assert_array_equal(D.detect("zf", inp).hard_labels, [0, 3])
+    for nv in (0.01, 0.5):
+        y = np.array([0.3 + 0.1j, -0.2 - 0.7j])
+        out = D.mmse_detect(D.DetectorInput(h=np.eye(2, dtype=complex), y=y, noise_var=nv,
+                                            constellation=q4))
+        np.testing.assert_allclose(out.soft, y / (1 + nv), rtol=1e-12)
+    rng = np.random.default_rng(8)
+    for _ in range(20):
+        h, y, _ = _rand(rng, 1, 6, 4, 16, 0.02)
+        inp = D.DetectorInput(h=h[0], y=y[0], noise_var=0.02, constellation=q16)
+        for name, mode in (("zf", "zf"), ("mmse", "mmse")):
+            out = D.detect(name, inp)
+            olab, ollr, osoft = orc.linear_detect(h, y, 0.02, 16, mode)
+            np.testing.assert_array_equal(out.hard_labels, olab[0])
+            np.testing.assert_allclose(out.llrs, ollr[0], rtol=0, atol=LLR_ATOL)
+            np.testing.assert_allclose(out.soft, osoft[0], rtol=1e-9)
+            np.testing.assert_allclose(out.hard, q16.points[olab[0]])
+    with pytest.raises(D.SingularChannelError):
+        D.zf_detect(D.DetectorInput(h=np.ones((2, 2), complex), y=np.ones(2, complex),
+                                    noise_var=0.1, constellation=q4))
+    with pytest.raises(D.SingularChannelError):
+        D.zf_detect(D.DetectorInput(h=np.ones((2, 3), complex), y=np.ones(2, complex),
+                                    noise_var=0.1, constellation=q4))
