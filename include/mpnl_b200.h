@@ -153,23 +153,24 @@ int mpnl_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t n_
  * uint8 (B,N) nearest points, llr float64 (B,N,log2 Q) clipped to +-clip,
  * optional est complex128 (B,N) raw equalised symbols A^-1 H^H y (the biased
  * MMSE output, detect.py:129-136; NULL skips), optional
- * device int32 *n_singular += vectors whose A had a Cholesky pivot below 64 ulp
- * of its diagonal entry, i.e. singular to working precision (the reference's np.linalg.inv raises LinAlgError there).
+ * device int32 *n_singular += vectors whose A had an exactly zero (or
+ * non-finite) Cholesky pivot, where the reference's np.linalg.inv (LAPACK
+ * getrf) raises LinAlgError.
  * Errors: unknown mode -> MPNL_EINVAL; N > 16 or Q not in {4,16,64} -> MPNL_EUNSUPPORTED. */
 int mpnl_linear_detect(const void* h, const void* y, int64_t n_vectors, int m, int n, int q,
                        int mode, double noise_var, const double* noise_var_per_vector,
                        double clip, uint8_t* labels_out, double* llr_out, void* est_out,
                        int32_t* n_singular, void* stream);
 
-/* Scale of the fp32 error bound used by the traversal guard (default 1 =
- * the rigorous bound; <= 0 restores the default).  Diagnostics only. */
-void mpnl_set_guard_scale(double c);
-
-/* Optional device int32[8] counters (NULL disables; diagnostics only): [0] events logged,
- * [1] guarded decisions re-decided in fp64, [2] two-way near-ties settled in
- * fp64, [3] vectors sent to the fp64 kernel, of which [4] three-way ties,
- * [5] fp64-level ties, [6] fp64 disagreements, [7] event-log overflows. */
-void mpnl_set_stats(int32_t* device_counters);
+/* Byte offset, inside the mpnl_detect_hard workspace, of eight int32
+ * diagnostic counters the last call on that workspace left (valid once the
+ * stream reaches the end of the call; reset by the next call): [0] events
+ * logged, [1] guarded decisions re-decided in fp64, [2] two-way near-ties
+ * settled in fp64, [3] vectors sent to the fp64 kernel, of which [4] three-way
+ * ties, [5] fp64-level ties, [6] fp64 disagreements, [7] event-log overflows.
+ * (There is no process-global state: all scratch lives in the caller's
+ * workspace.) */
+int64_t mpnl_workspace_stats_offset(void);
 
 /* FFMA throughput probe (for the roofline denominator): runs `iters` dependent
  * FFMA chains on every SM; returns FLOPs executed.  out: device float[blocks*threads]. */

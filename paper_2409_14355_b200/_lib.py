@@ -43,8 +43,7 @@ _SIGS = {
                             _i32),
     "mpnl_linear_detect": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _f64, _vp, _f64, _vp, _vp,
                             _vp, _vp, _vp], _i32),
-    "mpnl_set_guard_scale": ([_f64], None),
-    "mpnl_set_stats": ([_vp], None),
+    "mpnl_workspace_stats_offset": ([], _i64),
     "mpnl_ffma_probe": ([_vp, _i32, _i32, _i32, _vp], _i64),
     "mpnl_ffma2_probe": ([_vp, _i32, _i32, _i32, _vp], _i64),
 }

@@ -58,9 +58,7 @@ using namespace mpnl;
 
 namespace {
 
-thread_local std::string g_err;
-double g_guard_scale = 0.0;
-int32_t* g_stats = nullptr;
+thread_local std::string g_err;   // mpnl_last_error(): per calling thread
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -181,7 +179,7 @@ struct Workspace {
     B = std::max<int64_t>(B, 1);
     ev_cap = std::min<int64_t>(8 * B + 4096, int64_t(1) << 30);
     int64_t o = 0;
-    counters = o; o = up(o + 16);
+    counters = o; o = up(o + 64);   // 4 work counters + 8 diagnostic event counters
     fix_list = o; o = up(o + 8 * B);
     vflag = o; o = up(o + 4 * B);
     vres = o; o = up(o + 16 * B);
@@ -203,10 +201,6 @@ extern "C" {
 const char* mpnl_last_error(void) { return g_err.c_str(); }
 
 int mpnl_version(void) { return 0x000100; }
-
-void mpnl_set_guard_scale(double c) { g_guard_scale = c; }
-
-void mpnl_set_stats(int32_t* device_counters) { g_stats = device_counters; }
 
 int mpnl_alloc_expansions(int n_layers, int q, int64_t n_paths, int n_forced,
                           int64_t* expansions_out, int64_t* realized_out, int* warned) {
@@ -245,6 +239,8 @@ int mpnl_alloc_expansions(int n_layers, int q, int64_t n_paths, int n_forced,
 }
 
 int64_t mpnl_tables_floats(int m, int n) { return TableLayout(m, n).total; }
+
+int64_t mpnl_workspace_stats_offset(void) { return 16; }
 
 int64_t mpnl_workspace_bytes(int64_t n_vectors, int n, int q, const int64_t* expansions) {
   const int L = levels_for(q);
@@ -303,13 +299,13 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   a.zq = reinterpret_cast<float4*>(ws + W.zq);
   a.thrg = reinterpret_cast<float*>(ws + W.thrg);
   a.vaux = reinterpret_cast<float2*>(ws + W.vaux);
-  a.stats = g_stats;
+  a.stats = a.counters + 4;   // diagnostic counters (mpnl_workspace_stats)
   a.n_ch = n_ch;
   a.V = v_per_ch;
   a.m = m;
   a.ev_cap = (int)W.ev_cap;
   a.metric_offset = m > n;
-  a.guard_scale = (float)(g_guard_scale > 0 ? g_guard_scale : 1.0);
+  a.guard_scale = 1.0f;   // rigorous fp32 error bound
   // overloaded channels and trees with more than MPNL_XMAX expanded layers
   // (e.g. full enumeration) are detected entirely by the fp64 kernel
   const bool augmented = n > m;
@@ -317,7 +313,7 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
                     TravSmem(m, n, 4, MPNL_VPI_MAX, tp.list_bytes).total_bytes > 160 * 1024;
   cudaError_t e = cudaSuccess;
   if (stage == 1) {   // reset + partial-layer selection
-    e = cudaMemsetAsync(a.counters, 0, 16, st);
+    e = cudaMemsetAsync(a.counters, 0, 64, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.vflag, 0, 4 * B, st);
     if (e != cudaSuccess) return cuda_fail(e, "memset");
     if (slow) return MPNL_OK;
@@ -547,9 +543,17 @@ struct HostPipe {
   cudaStream_t up = nullptr, down = nullptr, cs[HOST_SLOTS];
   cudaEvent_t in_ready[HOST_SLOTS], done[HOST_SLOTS], out_done[HOST_SLOTS], fin, planned;
 };
-thread_local HostPipe g_pipe;
+// streams/events are device objects: one pipe per (calling thread, device)
+#define PIPE_MAX_DEV 16
+thread_local HostPipe g_pipes[PIPE_MAX_DEV];
+thread_local HostPipe* g_pipe_cur = nullptr;
+#define g_pipe (*g_pipe_cur)
 
 int pipe_init() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= PIPE_MAX_DEV)
+    return fail(MPNL_ECUDA, "host pipeline: no current CUDA device");
+  g_pipe_cur = &g_pipes[dev];
   if (g_pipe.init) return MPNL_OK;
   cudaError_t e = cudaStreamCreateWithFlags(&g_pipe.up, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g_pipe.down, cudaStreamNonBlocking);
@@ -694,9 +698,15 @@ struct GroupPipe {
   cudaStream_t gs[GROUP_MAX];
   cudaEvent_t fork, done[GROUP_MAX];
 };
-thread_local GroupPipe g_grp;
+thread_local GroupPipe g_grps[PIPE_MAX_DEV];   // per (calling thread, device)
+thread_local GroupPipe* g_grp_cur = nullptr;
+#define g_grp (*g_grp_cur)
 
 int group_init() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= PIPE_MAX_DEV)
+    return fail(MPNL_ECUDA, "group streams: no current CUDA device");
+  g_grp_cur = &g_grps[dev];
   if (g_grp.init) return MPNL_OK;
   int lo = 0, hi = 0;
   cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);   // hi = greatest priority

@@ -39,6 +39,7 @@
 namespace mpnl {
 
 #define EX_THREADS 256
+#define EX_KW 4   // 64-bit key words: 10 six-bit labels each, 40 >= MPNL_MAX_N streams
 #define EX_LIST_MAX (48 * 1024)
 
 struct ExLayout {   // dynamic shared memory (bytes)
@@ -66,7 +67,7 @@ struct ExLayout {   // dynamic shared memory (bytes)
     misc = o; o += 32;
     perm = o; o += 4 * MPNL_MAX_N;
     cand_m = o; o += 8 * EX_THREADS;
-    cand_k = o; o += 24 * EX_THREADS;
+    cand_k = o; o += 8 * EX_KW * EX_THREADS;
     cand_p = o; o += 4 * EX_THREADS;
     lists = o; o += (lb <= EX_LIST_MAX ? lb : 0);
     total = (o + 15) & ~15;
@@ -75,12 +76,13 @@ struct ExLayout {   // dynamic shared memory (bytes)
 
 // (metric, label key) total order: key words hold the stream-order labels,
 // stream 0 in the most significant bits (lexicographic = unsigned compare)
-__device__ __forceinline__ bool ex_key_less(double m1, const unsigned long long (&k1)[3],
-                                            double m2, const unsigned long long (&k2)[3]) {
+__device__ __forceinline__ bool ex_key_less(double m1, const unsigned long long (&k1)[EX_KW],
+                                            double m2, const unsigned long long (&k2)[EX_KW]) {
   if (m1 != m2) return m1 < m2;
-  if (k1[0] != k2[0]) return k1[0] < k2[0];
-  if (k1[1] != k2[1]) return k1[1] < k2[1];
-  return k1[2] < k2[2];
+#pragma unroll
+  for (int w = 0; w < EX_KW - 1; ++w)
+    if (k1[w] != k2[w]) return k1[w] < k2[w];
+  return k1[EX_KW - 1] < k2[EX_KW - 1];
 }
 
 // per-axis nearest level of c (ties -> lower Gray label): nearest_level_f64
@@ -367,7 +369,7 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
     // ---- 3. thread per path ----
     double bm = CUDART_INF;
     int bp = 0x7fffffff;
-    unsigned long long bk[3] = {~0ull, ~0ull, ~0ull};
+    unsigned long long bk[EX_KW] = {~0ull, ~0ull, ~0ull, ~0ull};
     // (rolled loops, residuals in local memory: the kernel runs for a few
     // vectors, so its cold instruction fetch, not its arithmetic, sets the
     // latency -- keep the code small)
@@ -375,7 +377,7 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
       double2 acc[N];
 #pragma unroll 1
       for (int k = 0; k < N; ++k) acc[k] = make_double2(0.0, 0.0);
-      unsigned long long key[3] = {0ull, 0ull, 0ull};
+      unsigned long long key[EX_KW] = {0ull, 0ull, 0ull, 0ull};
       double ped = 0.0, xs2 = 0.0;
 #pragma unroll 1
       for (int pos = N - 1; pos >= 0; --pos) {
@@ -403,9 +405,9 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
         const unsigned lab = (unsigned)((gray_code(ir) << h) | gray_code(ii));
         const int k = ps[pos];                              // stream index
         const int w = k / 10, sh = 6 * (9 - k % 10);
-        key[0] |= (w == 0) ? (unsigned long long)lab << sh : 0ull;
-        key[1] |= (w == 1) ? (unsigned long long)lab << sh : 0ull;
-        key[2] |= (w == 2) ? (unsigned long long)lab << sh : 0ull;
+#pragma unroll
+        for (int ww = 0; ww < EX_KW; ++ww)
+          key[ww] |= (w == ww) ? (unsigned long long)lab << sh : 0ull;
         if (a.full_labels) a.full_labels[(gv * P + p) * N + k] = (uint8_t)lab;
 #pragma unroll 2
         for (int kk = 0; kk < pos; ++kk) {
@@ -422,32 +424,39 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
       if (bp == 0x7fffffff || ex_key_less(met, key, bm, bk)) {
         bm = met;
         bp = p;
-        bk[0] = key[0]; bk[1] = key[1]; bk[2] = key[2];
+#pragma unroll
+        for (int ww = 0; ww < EX_KW; ++ww) bk[ww] = key[ww];
       }
     }
     // ---- 4. block argmin on (metric, labels) ----
     cm[tid] = bm;
     cp[tid] = bp;
-    ck[3 * tid] = bk[0]; ck[3 * tid + 1] = bk[1]; ck[3 * tid + 2] = bk[2];
+#pragma unroll
+    for (int ww = 0; ww < EX_KW; ++ww) ck[EX_KW * tid + ww] = bk[ww];
     __syncthreads();
     for (int s = EX_THREADS / 2; s > 0; s >>= 1) {
       if (tid < s) {
         const int o = tid + s;
-        const unsigned long long ko[3] = {ck[3 * o], ck[3 * o + 1], ck[3 * o + 2]};
-        const unsigned long long kt[3] = {ck[3 * tid], ck[3 * tid + 1], ck[3 * tid + 2]};
+        unsigned long long ko[EX_KW], kt[EX_KW];
+#pragma unroll
+        for (int ww = 0; ww < EX_KW; ++ww) {
+          ko[ww] = ck[EX_KW * o + ww];
+          kt[ww] = ck[EX_KW * tid + ww];
+        }
         const bool take = cp[o] != 0x7fffffff &&
                           (cp[tid] == 0x7fffffff || ex_key_less(cm[o], ko, cm[tid], kt));
         if (take) {
           cm[tid] = cm[o];
           cp[tid] = cp[o];
-          ck[3 * tid] = ko[0]; ck[3 * tid + 1] = ko[1]; ck[3 * tid + 2] = ko[2];
+#pragma unroll
+          for (int ww = 0; ww < EX_KW; ++ww) ck[EX_KW * tid + ww] = ko[ww];
         }
       }
       __syncthreads();
     }
     if (tid < N) {
       // winner label of stream `tid` from the key
-      const unsigned long long kw = ck[tid / 10];
+      const unsigned long long kw = ck[tid / 10];   // the winner's words (thread 0's slot)
       const uint8_t wl = (uint8_t)((kw >> (6 * (9 - tid % 10))) & 63u);
       // Fix-up mode: when the fp64 winner equals the fp32 winner, keep the
       // fp32 result untouched, so outputs never depend on which vectors a

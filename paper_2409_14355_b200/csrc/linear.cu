@@ -13,8 +13,9 @@
 // per-thread local memory, soft comes from two triangular solves and diag(A^-1)
 // from the column norms of L^-1.  Same quantities, different rounding: the
 // parity tests compare soft values and LLRs within a stated tolerance and the
-// hard labels exactly.  A pivot below 64 ulp of its diagonal entry marks the vector singular (the
-// reference's np.linalg.inv raises LinAlgError); the count goes to *n_singular.
+// hard labels exactly.  An exactly zero (or non-finite) pivot marks the vector
+// singular, where the reference's np.linalg.inv (LAPACK getrf) raises
+// LinAlgError; the count goes to *n_singular.
 //
 // One thread per vector: O(M N^2 + N^3) fp64 flops on 16 (M N + M) input bytes
 // per vector; vectors are independent.
@@ -24,7 +25,6 @@
 namespace {
 
 constexpr int kMaxN = 16;
-constexpr double kSingularTol = 64.0 * 2.220446049250313e-16;   // 64 ulp of a_jj
 
 struct cd { double re, im; };
 struct Tri {          // strided view: element e of this thread's triangle
@@ -91,11 +91,14 @@ linear_detect_kernel(const double2* __restrict__ h, const double2* __restrict__ 
   bool singular = false;
   for (int j = 0; j < n; ++j) {
     const Row rj{L, j * (j + 1) / 2};
-    const double ajj = rj[j].x;
-    double d = ajj;
+    double d = rj[j].x;
     for (int k = 0; k < j; ++k) d -= rj[k].x * rj[k].x + rj[k].y * rj[k].y;
-    // pivot at rounding level of the diagonal: A is singular to working precision
-    if (!(d > kSingularTol * ajj)) { singular = true; d = 1.0; }
+    // LAPACK getrf (np.linalg.inv) raises only on an exactly zero pivot: flag
+    // a zero / non-finite pivot; a rounding-level negative one goes on as |d|
+    // (A is then numerically singular and, as in the reference, the outputs
+    // are whatever the factorisation gives)
+    if (!(d != 0.0) || !isfinite(d)) { singular = true; d = 1.0; }
+    d = fabs(d);
     const double ljj = sqrt(d), inv = 1.0 / ljj;
     rj[j] = make_double2(ljj, 0.0);
     for (int i = j + 1; i < n; ++i) {
@@ -111,7 +114,7 @@ linear_detect_kernel(const double2* __restrict__ h, const double2* __restrict__ 
   if (singular && n_singular) atomicAdd(n_singular, 1);
   // forward L w = H^H y, back L^H soft = w
   for (int i = 0; i < n; ++i) {
-    const const Row ri{L, i * (i + 1) / 2};
+    const Row ri{L, i * (i + 1) / 2};
     double sr = x[i].re, si = x[i].im;
     for (int k = 0; k < i; ++k) {
       sr -= ri[k].x * x[k].re - ri[k].y * x[k].im;
@@ -178,8 +181,12 @@ linear_detect_kernel(const double2* __restrict__ h, const double2* __restrict__ 
     }
     labels_out[v * n + i] = (uint8_t)best_lab;
     double* lo = llr_out + (v * n + i) * bps;
-    for (int b = 0; b < bps; ++b)
-      lo[b] = fmin(fmax((d1[b] - d0[b]) / nv_eff, -clip), clip);
+    for (int b = 0; b < bps; ++b) {   // np.clip keeps NaN (fmin/fmax would not)
+      double l = (d1[b] - d0[b]) / nv_eff;
+      if (l < -clip) l = -clip;
+      if (l > clip) l = clip;
+      lo[b] = l;
+    }
   }
 }
 

@@ -232,13 +232,27 @@ def _shape_y(plan: BatchPathPlan, y):
     return yd.contiguous(), y64, was_np, squeeze
 
 
-def mpnl_detect_hard(plan: BatchPathPlan, h, y, c: Constellation, *, return_flags=False):
+def workspace_stats(ws: torch.Tensor) -> dict:
+    """The diagnostic counters a mpnl_detect_hard call left in its workspace."""
+    off = int(_lib.load().mpnl_workspace_stats_offset())
+    v = ws[off:off + 32].view(torch.int32).tolist()
+    keys = ("events", "redecided_fp64", "ties_settled_fp64", "sent_to_fp64", "three_way_ties",
+            "fp64_level_ties", "fp64_disagreements", "event_overflows")
+    return dict(zip(keys, v))
+
+
+def mpnl_detect_hard(plan: BatchPathPlan, h, y, c: Constellation, *, return_flags=False,
+                     workspace: torch.Tensor | None = None):
     """Hard-output MPNL: (hard labels (..., N), min_metric (...)).
 
     Equals `take_along_axis(labels, best)` / `metrics[best]` of
     `mpnl_detect_batch` (cli.py:236-239).  fp32 traversal kernel with an
     in-kernel guard; guarded vectors are recomputed in fp64 on the GPU.
-    `h` is accepted for signature parity (the metric uses the plan)."""
+    `h` is accepted for signature parity (the metric uses the plan).
+    `workspace`: optional caller-owned uint8 device buffer (reused across calls
+    on one stream; `workspace_stats` reads its counters); by default a fresh
+    one comes from the stream's caching allocator, so concurrent calls on
+    different streams never share scratch."""
     lib = _lib.load()
     if c.order != plan.order:
         raise ValueError("constellation does not match the plan")
@@ -249,8 +263,14 @@ def mpnl_detect_hard(plan: BatchPathPlan, h, y, c: Constellation, *, return_flag
     hard = torch.empty((nch, v, n), dtype=torch.uint8, device=dev)
     metric = torch.empty((nch, v), dtype=torch.float32, device=dev)
     flags = torch.empty((nch, v), dtype=torch.uint8, device=dev) if return_flags else None
-    ws = torch.empty(int(lib.mpnl_workspace_bytes(nch * v, n, c.order, plan.expansions.ctypes.data)),
-                     dtype=torch.uint8, device=dev)
+    nb = int(lib.mpnl_workspace_bytes(nch * v, n, c.order, plan.expansions.ctypes.data))
+    if nb < 0:
+        raise ValueError("unsupported configuration")
+    ws = workspace
+    if ws is None:
+        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    elif ws.numel() < nb or ws.device != dev or ws.dtype != torch.uint8:
+        raise ValueError(f"workspace must be a uint8 tensor of >= {nb} bytes on {dev}")
     rc = lib.mpnl_detect_hard(plan.perm_dev.data_ptr(), plan.r_dev.data_ptr(),
                               plan.qh_dev.data_ptr(), plan.tables.data_ptr(), yd.data_ptr(),
                               int(y64), nch, v, m, n, c.order, plan.expansions.ctypes.data,
@@ -281,9 +301,6 @@ def _host_complex(a, name):
     if arr.dtype != np.complex64:
         arr = arr.astype(np.complex128)
     return torch.from_numpy(np.ascontiguousarray(arr)), arr.dtype == np.complex128
-
-
-_HOST_WS: dict = {}
 
 
 def mpnl_hard_output(h, y, noise_var: float, n_paths: int, c: Constellation, *,
@@ -321,11 +338,9 @@ def mpnl_hard_output(h, y, noise_var: float, n_paths: int, c: Constellation, *,
                                            int(y64), ex.ctypes.data))
     if nb < 0:
         raise ValueError("unsupported configuration")
-    dev = _device()
-    ws = _HOST_WS.get(dev)
-    if ws is None or ws.numel() < nb:
-        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
-        _HOST_WS[dev] = ws
+    # per-call scratch from the caching allocator (the call synchronises below,
+    # so nothing outlives it; concurrent callers never share it)
+    ws = torch.empty(nb, dtype=torch.uint8, device=_device())
     rc = lib.mpnl_detect_hard_host(ht.data_ptr(), int(h64), yt.data_ptr(), int(y64), n_ch, v, m,
                                    n, c.order, ex.ctypes.data, float(noise_var), hard.data_ptr(),
                                    metric.data_ptr(), chunk_channels, ws.data_ptr(), ws.numel(),
@@ -333,9 +348,6 @@ def mpnl_hard_output(h, y, noise_var: float, n_paths: int, c: Constellation, *,
     _lib.check(rc, "mpnl_hard_output")
     torch.cuda.current_stream().synchronize()
     return hard, metric
-
-
-_GROUP_WS: dict = {}
 
 
 def mpnl_hard_output_device(h, y, noise_var: float, n_paths: int, c: Constellation, *,
@@ -362,10 +374,10 @@ def mpnl_hard_output_device(h, y, noise_var: float, n_paths: int, c: Constellati
     nb = int(lib.mpnl_group_workspace_bytes(n_ch, v, m, n, c.order, ex.ctypes.data, int(groups)))
     if nb < 0:
         raise ValueError("unsupported configuration")
-    ws = _GROUP_WS.get(yd.device)
-    if ws is None or ws.numel() < nb:
-        ws = torch.empty(nb, dtype=torch.uint8, device=yd.device)
-        _GROUP_WS[yd.device] = ws
+    # per-call scratch on the current stream: the forked group streams join back
+    # into it before the call returns, so the caching allocator's stream order
+    # protects the block when it is reused
+    ws = torch.empty(nb, dtype=torch.uint8, device=yd.device)
     rc = lib.mpnl_plan_detect_hard(hd.data_ptr(), int(h64), yd.data_ptr(), int(y64), n_ch, v, m,
                                    n, c.order, ex.ctypes.data, float(noise_var), hard.data_ptr(),
                                    metric.data_ptr(), int(groups), ws.data_ptr(), ws.numel(),

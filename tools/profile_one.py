@@ -17,13 +17,16 @@ c = constellation_for(cfg.order)
 h = torch.from_numpy(d["h"]).cuda()
 y = torch.from_numpy(d["y"]).cuda()
 from paper_2409_14355_b200 import _lib
-stats = torch.zeros(8, dtype=torch.int32, device="cuda")
-_lib.load().mpnl_set_stats(stats.data_ptr())
+lib = _lib.load()
+plan = det.mpnl_plan_batch(h, float(d["nv"][0]), cfg.n_paths, c)
+ws = torch.empty(int(lib.mpnl_workspace_bytes(y.shape[0] * y.shape[1], cfg.n, cfg.order,
+                                              plan.expansions.ctypes.data)),
+                 dtype=torch.uint8, device="cuda")
 for _ in range(reps):
     plan = det.mpnl_plan_batch(h, float(d["nv"][0]), cfg.n_paths, c)
-    hard, metric, flags = det.mpnl_detect_hard(plan, h, y, c, return_flags=True)
+    hard, metric, flags = det.mpnl_detect_hard(plan, h, y, c, return_flags=True, workspace=ws)
 torch.cuda.synchronize()
 nv_ = y.shape[0] * y.shape[1]
+st = det.workspace_stats(ws)
 print(name, "vectors", nv_, "flag rate", float(flags.float().mean()),
-      "per vector: events %.4f checked %.4f ties %.4f flagged %.5f [3way %.5f f64tie %.5f mismatch %.5f overflow %.5f]" % tuple(
-          x / reps / nv_ for x in stats.tolist()))
+      "per vector (last call):", {k: v / nv_ for k, v in st.items()})
