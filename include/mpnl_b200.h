@@ -172,6 +172,52 @@ int mpnl_linear_detect(const void* h, const void* y, int64_t n_vectors, int m, i
  * workspace.) */
 int64_t mpnl_workspace_stats_offset(void);
 
+/* ---- LDPC stage after detection (mpnlsim fec.py) ---- */
+
+/* Maximum check / variable degree of a dense m x n parity-check matrix H
+ * (host, row-major uint8).  MPNL_EINVAL unless 1 <= m < n ("parity-check
+ * matrix must be m x n with m < n"); MPNL_EUNSUPPORTED for degrees > 32 or
+ * >= 65535 edges.  Replaces LdpcCode.__post_init__ / _graph (fec.py:91-133). */
+int mpnl_ldpc_graph_dims(const uint8_t* H, int m, int n, int* max_dc, int* max_dv);
+
+/* Host: the decoder graph and the systematic encoder of H.
+ * check_vars (m*max_dc) uint16 variable of each check's slot, var_edges
+ * (n*max_dv) uint16 flat edge index (check*max_dc + slot) of each variable's
+ * slot — edges in np.nonzero order, 0xFFFF padding, as LdpcCode._graph
+ * (fec.py:107-133); encoder (m * ceil(k/32)) uint32 rows of E (bit j of word
+ * i = E[r, 32 i + j]), parity = E info mod 2 (fec.py:60-81, _encoder).
+ * MPNL_EINVAL "parity submatrix is singular" as the reference's ValueError. */
+int mpnl_ldpc_build(const uint8_t* H, int m, int n, int max_dc, int max_dv,
+                    uint16_t* check_vars, uint16_t* var_edges, uint32_t* encoder);
+
+/* Normalized min-sum decoding of n_words rate-matched words (replaces
+ * ldpc_decode, fec.py:156-220, and decode_rate_matched, fec.py:296-326), fp64,
+ * bit-identical to the reference.  Device: graph from mpnl_ldpc_build,
+ * llr_tx (n_words, n_tx) float64 (positive = bit 0); mother positions
+ * [0,k_tb) <- llr_tx[:, :k_tb], [k_tb,k) <- shortened_llr, [k,k+p) <-
+ * llr_tx[:, k_tb:], rest 0 (punctured), p = n_tx - k_tb (plain ldpc_decode:
+ * k_tb = k, n_tx = n).  Outputs: info_out (n_words, k_tb) uint8 bits of the
+ * hard decision at convergence (else after max_iter iterations), converged
+ * (n_words) uint8, iterations (optional, int32), *n_nonfinite (optional
+ * device int32) += words with a non-finite LLR (the reference raises
+ * ValueError("LLRs must be finite")). */
+int mpnl_ldpc_decode(const uint16_t* check_vars, const uint16_t* var_edges, int m, int n,
+                     int max_dc, int max_dv, const double* llr_tx, int64_t n_words, int n_tx,
+                     int k_tb, int max_iter, double alpha, double shortened_llr,
+                     uint8_t* info_out, uint8_t* converged, int32_t* iterations,
+                     int32_t* n_nonfinite, void* stream);
+
+/* Systematic (rate-matched) encoding (replaces ldpc_encode, fec.py:136-148,
+ * and encode_rate_matched, fec.py:278-293): info (n_words, k_tb) uint8 bits,
+ * zero-padded to k, tx_out (n_words, n_tx) = [info, parity[0, n_tx - k_tb)]. */
+int mpnl_ldpc_encode(const uint32_t* encoder, int m, int n, const uint8_t* info,
+                     int64_t n_words, int k_tb, int n_tx, uint8_t* tx_out, void* stream);
+
+/* Syndrome (n_words, m) uint8 of bits (n_words, n) (replaces ldpc_syndrome,
+ * fec.py:151-153). */
+int mpnl_ldpc_syndrome(const uint16_t* check_vars, int m, int max_dc, const uint8_t* bits,
+                       int64_t n_words, int n, uint8_t* syndrome_out, void* stream);
+
 /* FFMA throughput probe (for the roofline denominator): runs `iters` dependent
  * FFMA chains on every SM; returns FLOPs executed.  out: device float[blocks*threads]. */
 int64_t mpnl_ffma_probe(float* out, int blocks, int threads, int iters, void* stream);

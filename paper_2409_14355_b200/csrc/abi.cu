@@ -195,6 +195,10 @@ struct Workspace {
 
 }  // namespace
 
+namespace mpnl {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace mpnl
+
 // ------------------------------------------------------------------------------------------
 extern "C" {
 
