@@ -156,7 +156,7 @@ int mpnl_candidate_llrs(const uint8_t* labels, const double* metrics, int64_t n_
  * device int32 *n_singular += vectors whose A had an exactly zero (or
  * non-finite) Cholesky pivot, where the reference's np.linalg.inv (LAPACK
  * getrf) raises LinAlgError.
- * Errors: unknown mode -> MPNL_EINVAL; N > 16 or Q not in {4,16,64} -> MPNL_EUNSUPPORTED. */
+ * Errors: unknown mode -> MPNL_EINVAL; N > 32 or Q not in {4,16,64} -> MPNL_EUNSUPPORTED. */
 int mpnl_linear_detect(const void* h, const void* y, int64_t n_vectors, int m, int n, int q,
                        int mode, double noise_var, const double* noise_var_per_vector,
                        double clip, uint8_t* labels_out, double* llr_out, void* est_out,
@@ -217,6 +217,31 @@ int mpnl_ldpc_encode(const uint32_t* encoder, int m, int n, const uint8_t* info,
  * fec.py:151-153). */
 int mpnl_ldpc_syndrome(const uint16_t* check_vars, int m, int max_dc, const uint8_t* bits,
                        int64_t n_words, int n, uint8_t* syndrome_out, void* stream);
+
+/* ---- slot I/O around the detector (mpnlsim linksim.py) ---- */
+
+/* Receive grid y (frames, S, SC, m) = H x + noise per resource element
+ * (replaces linksim.py:207, einsum "tfmn,btfn->btfm" + noise): device
+ * complex128 h (S, SC, m, n), x (frames, S, SC, n), noise (frames, S, SC, m)
+ * or NULL. */
+int mpnl_slot_receive(const void* h, const void* x, const void* noise, int64_t frames,
+                      int symbols, int subcarriers, int m, int n, void* y, void* stream);
+
+/* DMRS least-squares channel estimate (replaces estimate_channel_ls,
+ * linksim.py:117-137): grid_obs (S, SC, m) complex128, pilots (n, n_pilot)
+ * complex128, port_symbol (n) int32 DMRS symbol of each stream, port_subcarriers
+ * (n, n_pilot) int32 its pilot subcarriers (device).  h_est (S, SC, m, n):
+ * obs / pilot (numpy's complex division, bit-identical) at the nearest pilot
+ * subcarrier (first minimum), the same for every symbol. */
+int mpnl_dmrs_ls_estimate(const void* grid_obs, const void* pilots, const int32_t* port_symbol,
+                          const int32_t* port_subcarriers, int symbols, int subcarriers, int m,
+                          int n, int n_pilot, void* h_est, void* stream);
+
+/* Gather the rows `rows` (device int32, n_rows) of a (batch, symbols, row)
+ * grid into (batch, n_rows, row): the per-RE flattening of the data symbols
+ * (h[data_syms], y[:, data_syms], linksim.py:211-216).  row_bytes % 16 == 0. */
+int mpnl_select_symbols(const void* src, int64_t batch, int symbols, int64_t row_bytes,
+                        const int32_t* rows, int n_rows, void* dst, void* stream);
 
 /* FFMA throughput probe (for the roofline denominator): runs `iters` dependent
  * FFMA chains on every SM; returns FLOPs executed.  out: device float[blocks*threads]. */

@@ -44,6 +44,9 @@ _SIGS = {
     "mpnl_linear_detect": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _f64, _vp, _f64, _vp, _vp,
                             _vp, _vp, _vp], _i32),
     "mpnl_workspace_stats_offset": ([], _i64),
+    "mpnl_slot_receive": ([_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp], _i32),
+    "mpnl_dmrs_ls_estimate": ([_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp], _i32),
+    "mpnl_select_symbols": ([_vp, _i64, _i32, _i64, _vp, _i32, _vp, _vp], _i32),
     "mpnl_ldpc_graph_dims": ([_vp, _i32, _i32, _vp, _vp], _i32),
     "mpnl_ldpc_build": ([_vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp], _i32),
     "mpnl_ldpc_decode": ([_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i64, _i32, _i32, _i32, _f64,

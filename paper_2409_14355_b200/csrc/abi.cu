@@ -490,7 +490,7 @@ int mpnl_linear_detect(const void* h, const void* y, int64_t n_vectors, int m, i
   if (mode != 0 && mode != 1)
     return fail(MPNL_EINVAL, "unknown linear mode " + std::to_string(mode));
   if (n < 1 || m < 1 || n_vectors < 0) return fail(MPNL_EINVAL, "inconsistent h/y dimensions");
-  if (n > linear_max_n()) return fail(MPNL_EUNSUPPORTED, "N > 16 streams is not supported");
+  if (n > linear_max_n()) return fail(MPNL_EUNSUPPORTED, "N > 32 streams is not supported");
   const int L = levels_for(q);
   if (!L) return fail(MPNL_EUNSUPPORTED, "unsupported constellation order " + std::to_string(q));
   const int half = q == 4 ? 1 : (q == 16 ? 2 : 3);

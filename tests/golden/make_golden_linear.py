@@ -24,6 +24,8 @@ from mpnlsim.core import constellation_for             # noqa: E402
 CASES = [  # (name, M, N, order, B)
     ("q4_2x2", 2, 2, 4, 64), ("q16_4x4", 4, 4, 16, 64), ("q64_8x8", 8, 8, 64, 32),
     ("q16_12x12", 12, 12, 16, 32), ("q4_6x4", 6, 4, 4, 64), ("q64_16x16", 16, 16, 64, 16),
+    # N > 16 (the C5 / C4 shapes and a ragged tall one), added in round 2
+    ("q64_24x24", 24, 24, 64, 16), ("q16_32x32", 32, 32, 16, 8), ("q16_28x19", 28, 19, 16, 16),
 ]
 
 

@@ -68,7 +68,8 @@ def test_gpu_linear_matches_reference_golden(mode):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["zf", "mmse"])
-@pytest.mark.parametrize("m,n,order", [(12, 12, 16), (4, 4, 64), (16, 8, 4), (16, 16, 16)])
+@pytest.mark.parametrize("m,n,order", [(12, 12, 16), (4, 4, 64), (16, 8, 4), (16, 16, 16),
+                                       (24, 24, 64), (32, 32, 16), (40, 17, 64), (9, 9, 4)])
 def test_gpu_linear_matches_oracle_random(mode, m, n, order):
     from paper_2409_14355_b200 import detect as D
     from paper_2409_14355_b200.core import constellation_for
@@ -77,7 +78,11 @@ def test_gpu_linear_matches_oracle_random(mode, m, n, order):
     lab, llr, est = D.linear_detect_batch(h, y, 0.03, constellation_for(order), mode,
                                           return_est=True)
     olab, ollr, oest = orc.linear_detect(h, y, 0.03, order, mode)
-    np.testing.assert_allclose(est, oest, rtol=1e-9, atol=1e-12)
+    # both sides solve A soft = H^H y in fp64 (LAPACK inverse there, Cholesky
+    # here): the difference is bounded by ~eps * cond(A) * |soft|
+    a = h.conj().transpose(0, 2, 1) @ h + (0.03 * np.eye(n) if mode == "mmse" else 0)
+    tol = 1e-9 + 8 * 2.2e-16 * np.linalg.cond(a)[:, None]
+    assert np.all(np.abs(est - oest) <= tol * np.abs(oest).max(axis=1, keepdims=True) + 1e-12)
     np.testing.assert_array_equal(lab, olab)
     np.testing.assert_allclose(llr, ollr, rtol=0, atol=LLR_ATOL)
 
@@ -110,6 +115,32 @@ def test_gpu_linear_reference_properties():
         D.linear_detect_batch(hs, np.ones((2, 2), complex), 0.1, q4, "zf")
     with pytest.raises(ValueError):
         D.linear_detect_batch(h, y, 0.1, q16, "lmmse")
+
+
+@pytest.mark.gpu
+def test_gpu_linear_nearly_dependent_columns_like_reference():
+    """A Gram matrix that is numerically near-singular but has no exactly zero
+    LU pivot: np.linalg.inv (the reference) returns without raising, so the
+    batch must not raise either (the old 64-ulp Cholesky test raised
+    here); an exactly singular one raises in both."""
+    from paper_2409_14355_b200 import detect as D
+    from paper_2409_14355_b200.core import constellation_for
+    q16 = constellation_for(16)
+    rng = np.random.default_rng(3)
+    h, y, _ = _rand(rng, 8, 4, 4, 16, 0.05)
+    h[3, :, 3] = h[3, :, 2] + 1e-7 * h[3, :, 1]       # cond(H^H H) ~ 1e14-1e16
+    gram = h.conj().transpose(0, 2, 1) @ h
+    np.linalg.inv(gram)                               # the reference's step: no raise
+    lab, llr = D.linear_detect_batch(h, y, 0.05, q16, "zf")
+    assert lab.shape == (8, 4)
+    olab, ollr, _ = orc.linear_detect(h[:3], y[:3], 0.05, 16, "zf")
+    np.testing.assert_array_equal(lab[:3], olab)      # the well-conditioned rows agree
+    hs = h.copy()
+    hs[0] = 0.0                                       # exactly singular
+    with pytest.raises(np.linalg.LinAlgError):
+        np.linalg.inv(hs.conj().transpose(0, 2, 1) @ hs)
+    with pytest.raises(np.linalg.LinAlgError):
+        D.linear_detect_batch(hs, y, 0.05, q16, "zf")
 
 
 @pytest.mark.gpu

@@ -47,9 +47,17 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
     byt = b * (16 * (m * n + m) + n * (1 + 8 * c.bits_per_symbol))
+    # algorithmic fp64 flops: Gram lower triangle 4MN(N+1) + H^H y 8MN + Cholesky
+    # 4N^3/3 + two triangular solves 8N^2 + diag(A^-1) via L^-1 4N^3/3
+    fl = b * (4 * m * n * (n + 1) + 8 * m * n + 8 * n ** 3 / 3 + 8 * n * n)
+    fp64_peak = 148 * 64 * 2 * 1.965e9
+    hbm = 6549.8e9
+    t = ms * 1e-3
     print(json.dumps({"kernel": "linear_detect_kernel", "mode": mode, "M": m, "N": n, "Q": q,
-                      "vectors": b, "ms": round(ms, 4), "vectors_per_s": b / ms * 1e3,
-                      "algorithmic_GBps": byt / ms / 1e6}))
+                      "vectors": b, "ms": round(ms, 4), "vectors_per_s": b / t,
+                      "algorithmic_GBps": byt / t / 1e9, "hbm_frac": round(byt / t / hbm, 4),
+                      "fp64_tflops": fl / t / 1e12, "fp64_frac": round(fl / t / fp64_peak, 4),
+                      "bound": "hbm" if byt / hbm > fl / fp64_peak else "fp64"}))
 
 
 if __name__ == "__main__":
