@@ -560,7 +560,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-s", type=float, default=15.0, help="cpu_baseline sample seconds")
-    ap.add_argument("--ref-step-s", type=float, default=4.0, help="reference arm s/step")
+    ap.add_argument("--ref-step-s", type=float, default=3.0, help="reference arm s/step")
     args = ap.parse_args(argv)
     if args.impl == "mpnl":
         args.warmup = max(args.warmup, 3)

@@ -132,6 +132,7 @@ class BatchPathPlan:
     noise_var: float = 0.0
     order: int = 0
     h_dev: torch.Tensor = field(default=None, repr=False)
+    h_src: object = field(default=None, repr=False, compare=False)   # the planned h object
 
     @property
     def batch(self) -> int:
@@ -200,7 +201,7 @@ def mpnl_plan_batch(h, noise_var: float, n_paths: int, c: Constellation) -> Batc
     _lib.check(rc, "mpnl_plan")
     return BatchPathPlan(perm_dev=perm, r_dev=r, qh_dev=qh, tables=tables,
                          expansions=expansions, n_paths=realized, augmented=n > m,
-                         noise_var=float(noise_var), order=c.order, h_dev=hd)
+                         noise_var=float(noise_var), order=c.order, h_dev=hd, h_src=h)
 
 
 def mpnl_preprocess(h, noise_var: float, n_paths: int, c: Constellation) -> PathPlan:
@@ -216,6 +217,28 @@ def mpnl_preprocess(h, noise_var: float, n_paths: int, c: Constellation) -> Path
 # ---------------------------------------------------------------------------
 # detection
 # ---------------------------------------------------------------------------
+
+def _check_h(plan: BatchPathPlan, h):
+    """The reference scores paths by ||y - H x||^2 with the `h` passed to
+    mpnl_detect_batch (detect.py:484-486); here the metric is the plan's PED,
+    which equals it exactly for the planned channel.  `h` must therefore be the
+    planned channel: the same object (free), or equal data (one device
+    comparison); another channel raises instead of silently mixing the two."""
+    if h is None or h is plan.h_src or h is plan.h_dev:
+        return
+    if isinstance(h, torch.Tensor):
+        t = h.to(plan.h_dev.device)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(h))).to(plan.h_dev.device)
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    ref = plan.h_dev
+    if tuple(t.shape) != tuple(ref.shape):
+        raise ValueError("inconsistent channel/observation dimensions")
+    if not torch.equal(t.to(torch.complex128), ref.to(torch.complex128)):
+        raise ValueError("h differs from the channel the plan was made for: "
+                         "re-plan with mpnl_plan_batch(h, ...)")
+
 
 def _shape_y(plan: BatchPathPlan, y):
     yd, y64, was_np = _to_dev_complex(y, "y")
@@ -248,7 +271,8 @@ def mpnl_detect_hard(plan: BatchPathPlan, h, y, c: Constellation, *, return_flag
     Equals `take_along_axis(labels, best)` / `metrics[best]` of
     `mpnl_detect_batch` (cli.py:236-239).  fp32 traversal kernel with an
     in-kernel guard; guarded vectors are recomputed in fp64 on the GPU.
-    `h` is accepted for signature parity (the metric uses the plan).
+    `h` must be the planned channel (`_check_h`: the metric is the plan's PED,
+    equal to the reference's true residual for that channel).
     `workspace`: optional caller-owned uint8 device buffer (reused across calls
     on one stream; `workspace_stats` reads its counters); by default a fresh
     one comes from the stream's caching allocator, so concurrent calls on
@@ -256,6 +280,7 @@ def mpnl_detect_hard(plan: BatchPathPlan, h, y, c: Constellation, *, return_flag
     lib = _lib.load()
     if c.order != plan.order:
         raise ValueError("constellation does not match the plan")
+    _check_h(plan, h)
     yd, y64, was_np, squeeze = _shape_y(plan, y)
     nch, v, m = yd.shape
     n = plan.n
@@ -396,6 +421,7 @@ def mpnl_detect_batch(plan: BatchPathPlan, h, y, c: Constellation):
     lib = _lib.load()
     if c.order != plan.order:
         raise ValueError("constellation does not match the plan")
+    _check_h(plan, h)
     yd, y64, was_np, squeeze = _shape_y(plan, y)
     nch, v, m = yd.shape
     n, p = plan.n, plan.n_paths

@@ -185,3 +185,23 @@ def test_invalid_arguments(det):
         det.mpnl_detect_hard(plan, None, np.zeros((2, 4), complex), QPSK)   # batch mismatch
     with pytest.raises(NotImplementedError):
         det.mpnl_plan_batch(rand_channel(rng, 33, 33)[None], 0.1, 8, QPSK)
+
+
+def test_detect_requires_the_planned_channel():
+    """The metric is the plan's PED, which is the reference's true residual
+    ||y - Hx||^2 (detect.py:484-486) for the PLANNED channel: the same channel
+    (object or equal data) is accepted, another one raises."""
+    import torch
+    from paper_2409_14355_b200 import detect as det
+    rng = np.random.default_rng(4)
+    h = (rng.standard_normal((3, 4, 4)) + 1j * rng.standard_normal((3, 4, 4))) / np.sqrt(2)
+    y = (rng.standard_normal((3, 5, 4)) + 1j * rng.standard_normal((3, 5, 4)))
+    plan = det.mpnl_plan_batch(h, 0.1, 16, QPSK)
+    a = det.mpnl_detect_hard(plan, h, y, QPSK)
+    b = det.mpnl_detect_hard(plan, h.copy(), y, QPSK)            # equal data: fine
+    c = det.mpnl_detect_hard(plan, torch.from_numpy(h).cuda(), y, QPSK)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[0], c[0])
+    with pytest.raises(ValueError, match="differs"):
+        det.mpnl_detect_hard(plan, 2 * h, y, QPSK)
+    with pytest.raises(ValueError, match="differs"):
+        det.mpnl_detect_batch(plan, 2 * h, y, QPSK)
