@@ -241,3 +241,23 @@ def test_device_one_call_matches_staged_path(name, n_rb):
         assert torch.equal(hd, ref_h) and torch.equal(md, ref_m), f"groups={g}"
     with pytest.raises(ValueError):
         det.mpnl_hard_output_device(h, y, nv, cfg.n_paths, c, groups=5)
+
+
+@pytest.mark.parametrize("m,n,order", [(8, 8, 16), (12, 12, 16), (16, 16, 64), (3, 5, 4)])
+def test_plan_kernels_bit_identical(m, n, order):
+    """Batches of >= 1024 small channels take the warp-per-channel plan kernel,
+    smaller ones the 4-warp-CTA kernel: both must give bit-identical plans
+    (same arithmetic order), so outputs never depend on the batch size."""
+    import torch
+    det = _det()
+    c = constellation_for(order)
+    rng = np.random.default_rng(m * 100 + n)
+    h = ((rng.standard_normal((1100, m, n)) + 1j * rng.standard_normal((1100, m, n)))
+         / np.sqrt(2)).astype(np.complex64)
+    big = det.mpnl_plan_batch(torch.from_numpy(h).cuda(), 0.3, 32, c)
+    small = det.mpnl_plan_batch(torch.from_numpy(h[:40]).cuda(), 0.3, 32, c)
+    # (the table blob mixes fp64 and fp32 fields: compare its bits)
+    for a, b in ((big.perm_dev, small.perm_dev), (big.r_dev, small.r_dev),
+                 (big.qh_dev, small.qh_dev),
+                 (big.tables.view(torch.int32), small.tables.view(torch.int32))):
+        assert torch.equal(a[:40], b), "plan kernels disagree"

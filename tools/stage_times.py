@@ -19,8 +19,11 @@ from paper_2409_14355_b200.workloads import CONFIGS, generate
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+pv = int(sys.argv[3]) if len(sys.argv) > 3 else 0   # > 0: pv instances, one channel each (V = 1)
 cfg = CONFIGS[name]
-d = generate(cfg)
+d = generate(cfg, n_rb=pv) if pv else generate(cfg)
+if pv:
+    d["y"] = np.ascontiguousarray(d["y"][:, :1])
 c = constellation_for(cfg.order)
 dev = torch.device("cuda", 0)
 stream = torch.cuda.Stream(dev)
