@@ -4,7 +4,8 @@
 //
 //   slot_receive:  y[b, t, f, :] = H[t, f] x[b, t, f] + noise[b, t, f]
 //                  (linksim.py:207, einsum "tfmn,btfn->btfm" + noise);
-//                  thread per (b, t, f, m), fp64 complex MACs over the N streams.
+//                  thread per (b, t, f, m), fp64 complex MACs over the N streams
+//                  in numpy's einsum order: bit-identical.
 //   dmrs_ls:       per stream v (DMRS symbol t_v, pilot subcarriers sc_v[p]):
 //                  h_pilot = obs[t_v, sc_v[p], :] / pilot_v[p] (numpy's complex
 //                  division, Smith's algorithm, bit for bit), nearest pilot
@@ -52,16 +53,18 @@ __global__ void slot_receive_kernel(const double2* __restrict__ h, const double2
     const int64_t b = i / ((int64_t)m * s * sc);
     const double2* hr = h + (tf * m + mm) * n;
     const double2* xr = x + (b * s * sc + tf) * n;
+    // numpy's einsum order: sequential over the streams from 0, each complex
+    // product's two real products rounded separately, then + noise (no FMA)
     double re = 0.0, im = 0.0;
     for (int k = 0; k < n; ++k) {
       const double2 a = hr[k], v = xr[k];
-      re += a.x * v.x - a.y * v.y;
-      im += a.x * v.y + a.y * v.x;
+      re = __dadd_rn(re, __dsub_rn(__dmul_rn(a.x, v.x), __dmul_rn(a.y, v.y)));
+      im = __dadd_rn(im, __dadd_rn(__dmul_rn(a.x, v.y), __dmul_rn(a.y, v.x)));
     }
     if (noise) {
       const double2 w = noise[i];
-      re += w.x;
-      im += w.y;
+      re = __dadd_rn(re, w.x);
+      im = __dadd_rn(im, w.y);
     }
     y[i] = make_double2(re, im);
   }

@@ -1,0 +1,45 @@
+"""Link-level frames on the GPU (simulate_frames: LDPC encode -> modulation ->
+DMRS -> receive grid -> genie or LS-DMRS CSI -> MPNL / ZF / MMSE soft output ->
+rate-matched LDPC decoding) against the reference's own simulate_frames
+(linksim.py:159-232) on the same seeded channel grids and per-frame random
+streams: the per-frame, per-stream decode outcomes must be identical
+(tests/golden/linksim.npz, make_golden_linksim.py)."""
+
+from fractions import Fraction
+from pathlib import Path
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+import linksim_cases as lc
+from paper_2409_14355_b200.core import constellation_for
+
+GOLD = np.load(Path(__file__).resolve().parent / "golden" / "linksim.npz")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", lc.CASES, ids=[c[0] for c in lc.CASES])
+def test_simulate_frames_matches_reference(case):
+    from paper_2409_14355_b200 import linksim as L
+    name, n, m, (q, rn, rd), rb, det, csi, p, snr, f = case
+    mcs = SimpleNamespace(constellation=constellation_for(q), code_rate=Fraction(rn, rd))
+    cfg = L.LinkConfig(n_streams=n, m_antennas=m, mcs=mcs, rb_per_vehicle=rb, detector=det,
+                       n_paths=p, csi=csi)
+    ok = L.simulate_frames(cfg, lc.channel(case), lc.noise_var(case), 3, range(f))
+    assert ok.shape == (f, n) and ok.dtype == bool
+    assert np.array_equal(ok, GOLD[name]), f"{name}: {int((ok != GOLD[name]).sum())} outcomes differ"
+
+
+def test_config_validation_like_reference():
+    from paper_2409_14355_b200 import linksim as L
+    mcs = SimpleNamespace(constellation=constellation_for(4), code_rate=Fraction(1, 2))
+    for kw in ({"n_streams": 13}, {"m_antennas": 0}, {"detector": "ml"}, {"csi": "perfect"}):
+        args = dict(n_streams=2, m_antennas=2, mcs=mcs, rb_per_vehicle=1)
+        args.update(kw)
+        with pytest.raises(ValueError):
+            L.LinkConfig(**args)
+    cfg = L.LinkConfig(n_streams=2, m_antennas=4, mcs=mcs, rb_per_vehicle=3)
+    assert cfg.n_subcarriers == 36 and cfg.bits_per_block == 36 * 12 * 2
+    with pytest.raises(ValueError, match="smaller"):
+        L.simulate_frames(cfg, np.zeros((14, 12, 4, 2), complex), 0.1, 0, range(1))
