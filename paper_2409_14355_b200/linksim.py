@@ -16,6 +16,7 @@ simulate_frames          linksim.py:159-232 (one channel, many frames)  all of t
                                                                         encode / decode + MPNL
                                                                         soft output / linear
 LinkConfig               linksim.py:31-65 (fields the frames use)       host
+PerResult, measure_per   linksim.py:83-96, 241-271 (PER + early stop)   simulate_frames
 =======================  =============================================  =========================
 
 `simulate_frames` keeps the reference's per-frame random streams (info bits and
@@ -291,3 +292,45 @@ def simulate_frames(cfg, grid, noise_var: float, chan_idx: int, frame_indices) -
     dec, conv = _fec.decode_rate_matched(code, rm, llrs_v)
     ok = conv.bool() & ~torch.any(dec != info_d, dim=1)
     return ok.reshape(f, n).cpu().numpy()
+
+
+@dataclass(frozen=True)
+class PerResult:
+    """Transport-block error count (linksim.py:83-96)."""
+    frames: int
+    errors: int
+
+    @property
+    def per(self) -> float:
+        return self.errors / self.frames
+
+    @property
+    def ci95_halfwidth(self) -> float:
+        p = self.per
+        return 1.96 * np.sqrt(max(p * (1 - p), 1e-12) / self.frames)
+
+
+def measure_per(cfg, channels, noise_vars, frames_per_channel: int = 200,
+                stop_threshold: float | None = None, min_frames: int = 400) -> PerResult:
+    """Average transport-block error rate over a channel set (linksim.py:241-271):
+    the reference's loop — 25-frame batches per channel, optional early stop
+    once the 95% interval excludes `stop_threshold` — over the GPU
+    `simulate_frames`; same frame indices, so the same outcomes."""
+    if frames_per_channel < 1:
+        raise ValueError("need at least one frame per channel")
+    frames = errors = 0
+    batch = 25
+    for chan_idx, (grid, nv) in enumerate(zip(channels, noise_vars)):
+        done = 0
+        while done < frames_per_channel:
+            take = min(batch, frames_per_channel - done)
+            ok = simulate_frames(cfg, grid, nv, chan_idx, range(done, done + take))
+            errors += int((~ok).sum())
+            frames += ok.size
+            done += take
+            if stop_threshold is not None and frames >= min_frames:
+                res = PerResult(frames=frames, errors=errors)
+                if (res.per - res.ci95_halfwidth > stop_threshold
+                        or res.per + res.ci95_halfwidth < stop_threshold):
+                    return res
+    return PerResult(frames=frames, errors=errors)

@@ -36,6 +36,21 @@ def main():
                                      lc.noise_var(case), 3, range(f))
         out[name] = ok
         print(name, ok.mean(), ok.shape)
+    # measure_per over two channels with the early stop armed (linksim.py:241-271)
+    case = lc.CASES[0]
+    name, n, m, (q, rn, rd), rb, det, csi, p, snr, f = case
+    mcs = next(e for e in core.MCS_TABLE
+               if e.modulation_order == q and e.code_rate == Fraction(rn, rd))
+    cfg = linksim.LinkConfig(n_streams=n, m_antennas=m, mcs=mcs, detector=det, n_paths=p,
+                             rb_per_vehicle=rb, csi=csi)
+    grids = [channel.ChannelGrid(h=lc.channel(case)),
+             channel.ChannelGrid(h=np.ascontiguousarray(lc.channel(case)[:, ::-1]))]
+    nvs = [lc.noise_var(case), 0.8 * lc.noise_var(case)]
+    r = linksim.measure_per(cfg, grids, nvs, frames_per_channel=60)
+    r2 = linksim.measure_per(cfg, grids, nvs, frames_per_channel=200, stop_threshold=0.9,
+                             min_frames=100)
+    out["measure_per"] = np.array([r.frames, r.errors, r2.frames, r2.errors])
+    print("measure_per", out["measure_per"])
     np.savez_compressed(HERE / "linksim.npz", **out)
 
 

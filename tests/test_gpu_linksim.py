@@ -43,3 +43,22 @@ def test_config_validation_like_reference():
     assert cfg.n_subcarriers == 36 and cfg.bits_per_block == 36 * 12 * 2
     with pytest.raises(ValueError, match="smaller"):
         L.simulate_frames(cfg, np.zeros((14, 12, 4, 2), complex), 0.1, 0, range(1))
+
+
+def test_measure_per_matches_reference():
+    """measure_per (linksim.py:241-271) over two channels, plain and with the
+    early stop armed: the same frames and errors as the reference."""
+    from paper_2409_14355_b200 import linksim as L
+    case = lc.CASES[0]
+    name, n, m, (q, rn, rd), rb, det, csi, p, snr, f = case
+    mcs = SimpleNamespace(constellation=constellation_for(q), code_rate=Fraction(rn, rd))
+    cfg = L.LinkConfig(n_streams=n, m_antennas=m, mcs=mcs, rb_per_vehicle=rb, detector=det,
+                       n_paths=p, csi=csi)
+    grids = [lc.channel(case), np.ascontiguousarray(lc.channel(case)[:, ::-1])]
+    nvs = [lc.noise_var(case), 0.8 * lc.noise_var(case)]
+    r = L.measure_per(cfg, grids, nvs, frames_per_channel=60)
+    r2 = L.measure_per(cfg, grids, nvs, frames_per_channel=200, stop_threshold=0.9,
+                       min_frames=100)
+    assert [r.frames, r.errors, r2.frames, r2.errors] == GOLD["measure_per"].tolist()
+    with pytest.raises(ValueError):
+        L.measure_per(cfg, grids, nvs, frames_per_channel=0)
