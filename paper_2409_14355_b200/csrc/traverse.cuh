@@ -72,7 +72,7 @@ struct DetectArgs {
 #define MPNL_VPI_MAX 8          // vectors per warp item in VPI mode
 #define MPNL_MAGIC 12582912.0f  // 1.5 * 2^23: fma(acc, kx, MAGIC) rounds x to an integer
 #define MPNL_U 5.9604645e-08f   // 2^-24
-#define EV_NODE 0
+#define EV_NODE 0   // (a NODE event's .w carries -evp: negative, see ev_node_w)
 #define EV_CUT 1
 #define TRAV_EV_CAP 256         // per-CTA event buffer of the traversal kernel
 #define MPNL_XS_STRIDE 128      // = traversal threads per CTA (per-thread symbol slots)
@@ -450,6 +450,18 @@ struct TravCfg {
   static constexpr int MB = N <= 8 ? MPNL_MINB_SMALL : (N <= 16 ? MPNL_MINB_MID : MPNL_MINB_LARGE);
   static constexpr int MINB = MB ? MB : (PT * N <= 24 ? 4 : 3);   // CTAs per SM (no spills)
 };
+
+// A NODE event's type word is the NEGATED lower bound evp of the path's PED
+// prefix at its first marked layer (sign bit set, so never equal to EV_CUT /
+// EV_TIE): the check kernel drops the event before any re-trace when evp
+// already exceeds the vector's final bound.
+__device__ __forceinline__ int ev_node_w(float evp) {
+  return (int)(__float_as_uint(evp) | 0x80000000u);
+}
+__device__ __forceinline__ bool ev_is_node(int w) { return w < 0; }
+__device__ __forceinline__ float ev_node_evp(int w) {
+  return __uint_as_float((unsigned)w & 0x7fffffffu);
+}
 
 // mark vector gv for the fp64 kernel (the first marker appends it to the list)
 // reasons (stats[4 + reason]): 0 three-way tie, 1 fp64-level tie, 2 fp64
@@ -1338,7 +1350,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
           if (ok[t] && evm[t] != 0u) {
             const float bnd = (wbest == INF) ? INF : wbest + 2.f * ped_tol(wbest, weacc[0], N);
             if (evp[t] <= bnd) {
-              const int4 e4 = make_int4(pp[t], (int)evm[t], gbase + vl[t], EV_NODE);
+              const int4 e4 = make_int4(pp[t], (int)evm[t], gbase + vl[t], ev_node_w(evp[t]));
               const int idx = atomicAdd(evn, 1);
               if (idx < TRAV_EV_CAP) evb[idx] = e4;
               else log_event(a, e4);
@@ -1793,32 +1805,35 @@ check_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
       const uint8_t* vlist = a.lists + gv * tp.list_bytes;
       const float4 res = a.vres[gv];
       const float lim = res.x + 2.f * ped_tol(res.x, res.w, N);
-      if (e4.w == EV_NODE) {
-        const unsigned mask = (unsigned)e4.y;
-        const int lowest = __ffs(mask) - 1;
-        warp_retrace<N, L>(T, zrow, vlist, tp, e4.x, lowest, lab, pre);
-        bool zdone = false;
-        double zr = 0.0, zi = 0.0;
-        for (int pos = N - 1; pos >= lowest; --pos) {
-          if (!((mask >> pos) & 1u) || pre[pos] > lim) continue;
-          if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
-          if (!zdone) { warp_z_f64(a, tab, gv, N, zr, zi); zdone = true; }
-          double cr, ci;
-          warp_centre_f64(a, c, N, L, pos, lab, zr, zi, cr, ci);
-          const int ir = nearest_level_f64(cr, L, nrm), ii = nearest_level_f64(ci, L, nrm);
-          if (ir * 8 + ii != lab[pos]) {
-            // the reference takes the other branch here.  Our fp32 path is then
-            // a candidate the reference lacks: harmless unless it is one of our
-            // two best.  The reference's path instead: harmless unless its exact
-            // metric could beat our winner.
-            const int2 pth = a.vpath[gv];
-            bool bad = e4.x == pth.x || e4.x == pth.y;
-            if (!bad) {
-              const double malt = warp_sic_f64(a, c, N, L, pos, lab, ir, ii, zr, zi);
-              bad = malt <= (double)lim;
+      if (ev_is_node(e4.w)) {
+        // every marked layer's prefix is >= evp: nothing can compete, no re-trace
+        if (ev_node_evp(e4.w) <= lim) {
+          const unsigned mask = (unsigned)e4.y;
+          const int lowest = __ffs(mask) - 1;
+          warp_retrace<N, L>(T, zrow, vlist, tp, e4.x, lowest, lab, pre);
+          bool zdone = false;
+          double zr = 0.0, zi = 0.0;
+          for (int pos = N - 1; pos >= lowest; --pos) {
+            if (!((mask >> pos) & 1u) || pre[pos] > lim) continue;
+            if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
+            if (!zdone) { warp_z_f64(a, tab, gv, N, zr, zi); zdone = true; }
+            double cr, ci;
+            warp_centre_f64(a, c, N, L, pos, lab, zr, zi, cr, ci);
+            const int ir = nearest_level_f64(cr, L, nrm), ii = nearest_level_f64(ci, L, nrm);
+            if (ir * 8 + ii != lab[pos]) {
+              // the reference takes the other branch here.  Our fp32 path is then
+              // a candidate the reference lacks: harmless unless it is one of our
+              // two best.  The reference's path instead: harmless unless its exact
+              // metric could beat our winner.
+              const int2 pth = a.vpath[gv];
+              bool bad = e4.x == pth.x || e4.x == pth.y;
+              if (!bad) {
+                const double malt = warp_sic_f64(a, c, N, L, pos, lab, ir, ii, zr, zi);
+                bad = malt <= (double)lim;
+              }
+              if (bad && lane == 0) send_to_fp64(a, gv, 2);
+              break;
             }
-            if (bad && lane == 0) send_to_fp64(a, gv, 2);
-            break;
           }
         }
       } else if (e4.w == EV_CUT) {
