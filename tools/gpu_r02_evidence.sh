@@ -1,0 +1,15 @@
+# Round-2 evidence on one B200 (run through gpurun from the repo root); outputs
+# land in gpurun_out/ and the committed copies in profiles/r02/.
+#   /usr/local/graft/bin/gpurun --timeout 3600 -- 'bash tools/gpu_r02_evidence.sh'
+set -u
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/e_smoke.log 2>&1; echo smoke rc=$?
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/e_gpu_tests.log 2>&1; echo tests rc=$?
+tail -2 gpurun_out/e_gpu_tests.log
+timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/e_bench_default.json 2> gpurun_out/e_bench_default.err; echo bench rc=$?
+timeout 1200 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/e_bench_reference.json 2>&1; echo ref rc=$?
+for c in C1 C2 C3 C4; do
+  timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-sweep > gpurun_out/e_bench_$c.json 2>/dev/null; echo $c rc=$?
+done
+for c in C5P1024 C5P256 C5P64 C5P16 C2 C3 C4 C1; do python tools/stage_times.py $c 10; done > gpurun_out/e_stage_times.txt 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/e_launches_default.csv \
+    python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu-baseline > /dev/null 2>&1; echo launches rc=$?
