@@ -1081,6 +1081,7 @@ prep2_kernel(const DetectArgs a, const TreeParams tp, int chunks, int pos_sel) {
 struct TravSmem {
   int tpo, tab, wbuf, bufsz, zs, thr, lst, eac, mbar, xs, ev, evn, total_bytes;   // floats / bytes
   int ck, cv;   // items and vectors per chunk
+  int tab0, tabn;   // staged slice of the channel's table blob (per-layer float4 + r'' columns)
   __host__ __device__ TravSmem(int m, int n, int warps, int nvi, int list_bytes) {
     TableLayout tl(m, n);
     const int npp = (n + 1) / 2, n4 = (n + 3) & ~3;
@@ -1100,7 +1101,9 @@ struct TravSmem {
     bufsz = eac + TableLayout::up4(2 * (cv + 2));
     int o = 0;
     tpo = o; o += TableLayout::up4((int)(sizeof(TreeParams) / 4));
-    tab = o; o += tl.total;
+    tab0 = tl.off_lay;                             // Q^H and the shift are not read here
+    tabn = tl.total - tl.off_lay;
+    tab = o; o += tabn;
     wbuf = o; o += warps * 2 * bufsz;
     mbar = o; o += warps * 2 * 2;                  // u64 mbarrier per warp buffer
     xs = o; o += 2 * MPNL_XMAX * MPNL_PT_SMALL * MPNL_XS_STRIDE;   // u64 per-thread symbols
@@ -1173,7 +1176,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const float INF = __int_as_float(0x7f800000);
   TreeParams& tp = *reinterpret_cast<TreeParams*>(sm + so.tpo);
-  float* tab = sm + so.tab;
+  float* tab = sm + so.tab - so.tab0;   // virtual blob base: only [tab0, total) is staged
   float* wb0 = sm + so.wbuf + warp * 2 * so.bufsz;
   uint64_t* wbar = reinterpret_cast<uint64_t*>(sm + so.mbar) + 2 * warp;
   if (lane == 0) {
@@ -1259,9 +1262,9 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     }
     __syncthreads();   // previous segment's tables no longer in use (and xs / tp ready)
     {
-      const float4* src = reinterpret_cast<const float4*>(a.tables + (int64_t)c * tl.total);
-      float4* dst = reinterpret_cast<float4*>(tab);
-      for (int i = tid; i < tl.total / 4; i += nth) dst[i] = src[i];
+      const float4* src = reinterpret_cast<const float4*>(a.tables + (int64_t)c * tl.total + so.tab0);
+      float4* dst = reinterpret_cast<float4*>(sm + so.tab);
+      for (int i = tid; i < so.tabn / 4; i += nth) dst[i] = src[i];
     }
     __syncthreads();
     for (; ch < nchunk; ++ch, k ^= 1) {

@@ -245,9 +245,9 @@ def test_device_one_call_matches_staged_path(name, n_rb):
 
 @pytest.mark.parametrize("m,n,order", [(8, 8, 16), (12, 12, 16), (16, 16, 64), (3, 5, 4)])
 def test_plan_kernels_bit_identical(m, n, order):
-    """Batches of >= 1024 small channels take the warp-per-channel plan kernel,
-    smaller ones the 4-warp-CTA kernel: both must give bit-identical plans
-    (same arithmetic order), so outputs never depend on the batch size."""
+    """Plans never depend on the batch size: channels of m (+ n) <= 32 rows all
+    take the register-resident lane-group kernel (one arithmetic order whatever
+    the number of channels, groups per warp or CTAs)."""
     import torch
     det = _det()
     c = constellation_for(order)
