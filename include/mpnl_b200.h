@@ -15,6 +15,9 @@
  *                              and test_acceptance.py:114-117)
  *   mpnl_detect_full       <- mpnl_detect_batch      detect.py:473-488
  *   mpnl_candidate_llrs    <- _candidate_llrs_batch  detect.py:439-453
+ *   mpnl_detect_llrs_fast  <- mpnl_detect_batch + _candidate_llrs_batch, the link
+ *                             simulator's MPNL soft output (linksim.py:151-155),
+ *                             in fp32 without the candidate list
  *   mpnl_linear_detect     <- linear_detect_batch    detect.py:528-557
  * INTEGRATION.md shows the ctypes binding a maintainer adds to detect.py.
  */
@@ -132,6 +135,28 @@ int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64,
                      const int64_t* expansions, double noise_var,
                      uint8_t* labels, double* metrics, int64_t* best,
                      void* stream);
+
+/* fp32 list max-log LLRs fused with the path traversal: the MPNL soft output
+ * of the link simulator (linksim.py:151-155 = mpnl_detect_batch, detect.py:473-488,
+ * then _candidate_llrs_batch, detect.py:439-453) without materialising the
+ * candidate list.  Plan and observation arguments as mpnl_detect_hard;
+ * llr_noise_var and clip are _candidate_llrs_batch's noise_var and clip.
+ * llr_out (B, n, log2 q) float64 and flags_out (B,) uint8 are device buffers.
+ * Path metrics are the traversal's fp32 PEDs: an LLR differs from the
+ * reference's by at most 2 ped_tol / noise_var (about 1e-6 relative to the
+ * metrics).  flags_out[b] = 1 marks a vector in which an fp32 decision within
+ * the guard bound of a decision boundary sits on a path that can reach an
+ * unclipped LLR: recompute those vectors with mpnl_detect_full +
+ * mpnl_candidate_llrs (the Python shim does) and every LLR is then the
+ * reference's within that tolerance.
+ * Errors: overloaded channels (n > m) and plans with more than 3 expanded layers
+ * have no fp32 path -> MPNL_EUNSUPPORTED. */
+int mpnl_detect_llrs_fast(const int32_t* perm, const void* r64, const void* qh64,
+                          const float* tables, const void* y, int y_is_f64, int64_t n_ch,
+                          int64_t v_per_ch, int m, int n, int q, const int64_t* expansions,
+                          double noise_var, double llr_noise_var, double clip, double* llr_out,
+                          uint8_t* flags_out, void* workspace, int64_t workspace_bytes,
+                          void* stream);
 
 /* List max-log LLRs over a candidate list (replaces _candidate_llrs_batch,
  * detect.py:439-453; bits as bits_from_labels, core.py:209-213, MSB first).

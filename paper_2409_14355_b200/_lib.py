@@ -36,6 +36,8 @@ _SIGS = {
                                _vp, _vp, _i64, _vp, _i64, _vp], _i32),
     "mpnl_detect_full": ([_vp, _vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _vp, _f64,
                           _vp, _vp, _vp, _vp], _i32),
+    "mpnl_detect_llrs_fast": ([_vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _vp,
+                               _f64, _f64, _f64, _vp, _vp, _vp, _i64, _vp], _i32),
     "mpnl_group_workspace_bytes": ([_i64, _i64, _i32, _i32, _i32, _vp, _i32], _i64),
     "mpnl_plan_detect_hard": ([_vp, _i32, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _vp, _f64,
                                _vp, _vp, _i32, _vp, _i64, _vp], _i32),

@@ -430,6 +430,89 @@ int mpnl_detect_hard(const int32_t* perm, const void* r64, const void* qh64, con
   return MPNL_OK;
 }
 
+}  // extern "C"
+
+// soft path: vectors whose partial-layer selection was a near-tie (EV_CUT events of
+// the prep / select kernels) or that the event log dropped go to the fp64 list path
+__global__ void soft_flag_kernel(const int4* __restrict__ events, const int32_t* __restrict__ counters,
+                                 int ev_cap, const uint32_t* __restrict__ vflag, int64_t B,
+                                 uint8_t* __restrict__ flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int nev = min(counters[1], ev_cap);
+  for (int64_t k = i; k < nev; k += stride) {
+    const int4 e = events[k];
+    if (e.w == EV_CUT) flags[(unsigned)e.z] = 1;
+  }
+  for (int64_t k = i; k < B; k += stride)
+    if (vflag[k]) flags[k] = 1;
+}
+
+extern "C" {
+
+int mpnl_detect_llrs_fast(const int32_t* perm, const void* r64, const void* qh64,
+                          const float* tables, const void* y, int y_is_f64, int64_t n_ch,
+                          int64_t v_per_ch, int m, int n, int q, const int64_t* expansions,
+                          double noise_var, double llr_noise_var, double clip, double* llr,
+                          uint8_t* flags, void* workspace, int64_t workspace_bytes,
+                          void* stream) {
+  if (int rc = check_dims(m, n, q)) return rc;
+  const int L = levels_for(q);
+  const int64_t B = n_ch * v_per_ch;
+  if (n_ch < 0 || v_per_ch < 0) return fail(MPNL_EINVAL, "negative batch");
+  if (!(llr_noise_var > 0)) return fail(MPNL_EINVAL, "noise_var must be positive");
+  if (B == 0) return MPNL_OK;
+  if (B > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "more than 2^31 vectors per call");
+  TreeBuild tb = build_tree(n, L, expansions);
+  if (!tb.ok) return fail(MPNL_EINVAL, tb.err);
+  const TreeParams& tp = tb.tp;
+  if (n > m || tp.n_top > MPNL_XMAX ||
+      TravSmem(m, n, 4, MPNL_VPI_MAX, tp.list_bytes).total_bytes > 160 * 1024)
+    return fail(MPNL_EUNSUPPORTED,
+                "no fp32 path for this plan (overloaded channel or > 3 expanded layers): "
+                "use mpnl_detect_full + mpnl_candidate_llrs");
+  // reset + rotation + guard thresholds + partial-layer selection, as for the hard output
+  if (int rc = mpnl_detect_hard_stage(1, perm, r64, qh64, tables, y, y_is_f64, n_ch, v_per_ch, m,
+                                      n, q, expansions, noise_var, nullptr, nullptr, nullptr,
+                                      workspace, workspace_bytes, stream))
+    return rc;
+  const Workspace W(B, tp.list_bytes, n);
+  char* ws = reinterpret_cast<char*>(workspace);
+  DetectArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.tables = tables;
+  a.y = y;
+  a.y_f64 = y_is_f64;
+  a.perm = perm;
+  a.r64 = (const double2*)r64;
+  a.qh64 = (const double2*)qh64;
+  a.counters = reinterpret_cast<int32_t*>(ws + W.counters);
+  a.vflag = reinterpret_cast<uint32_t*>(ws + W.vflag);
+  a.events = reinterpret_cast<int4*>(ws + W.events);
+  a.ev_cap = (int)W.ev_cap;
+  a.lists = reinterpret_cast<uint8_t*>(ws + W.lists);
+  a.zq = reinterpret_cast<float4*>(ws + W.zq);
+  a.thrg = reinterpret_cast<float*>(ws + W.thrg);
+  a.vaux = reinterpret_cast<float2*>(ws + W.vaux);
+  a.n_ch = n_ch;
+  a.V = v_per_ch;
+  a.m = m;
+  a.soft.llr = llr;
+  a.soft.flags = flags;
+  a.soft.noise_var = llr_noise_var;
+  a.soft.clip = clip;
+  a.soft.vc = 8;   // vectors per CTA (two per warp): the 5 KB table slice is staged per CTA
+  a.soft.chunks = (int)((v_per_ch + a.soft.vc - 1) / a.soft.vc);
+  if (n_ch * (int64_t)a.soft.chunks > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
+  cudaError_t e = launch_fast(n, L, 6, a, tp, 0, 128, 0, 0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "soft llr kernel");
+  soft_flag_kernel<<<148 * 4, 256, 0, (cudaStream_t)stream>>>(a.events, a.counters, a.ev_cap, a.vflag,
+                                                            B, flags);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "soft flag kernel");
+  return MPNL_OK;
+}
+
 int mpnl_detect_full(const int32_t* perm, const void* r64, const void* qh64, const void* y,
                      int y_is_f64, int64_t n_ch, int64_t v_per_ch, int m, int n, int q,
                      const int64_t* expansions, double noise_var, uint8_t* labels,

@@ -39,6 +39,16 @@
 
 namespace mpnl {
 
+// Soft-output (fp32 list max-log LLR) kernel arguments (soft.cuh)
+struct SoftArgs {
+  double* llr;        // (B, N, bps) fp64, stream order
+  uint8_t* flags;     // (B,) 1 = recompute in fp64
+  double noise_var;
+  double clip;
+  int vc;             // vectors per CTA
+  int chunks;         // CTAs per channel
+};
+
 struct DetectArgs {
   const float* tables;      // (n_ch, T) per channel blob (TableLayout)
   const void* y;            // (n_ch, V, M) complex64 or complex128
@@ -66,6 +76,7 @@ struct DetectArgs {
   int vpi, bpv;             // vectors per warp item (VPI mode) / path batches per vector
   int metric_offset;        // 1 when M > N: add ||y||^2 - ||z||^2
   float guard_scale;        // scales the fp32 error bound (1 = rigorous)
+  SoftArgs soft;            // soft_llr_kernel only
 };
 
 #define MPNL_XMAX 3             // expanded (e > 1) layers handled by the fast path

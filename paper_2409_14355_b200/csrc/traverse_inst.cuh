@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "traverse.cuh"
+#include "soft.cuh"
 
 #ifndef MPNL_TRAV_WAVES
 #define MPNL_TRAV_WAVES 4
@@ -17,7 +18,7 @@
 namespace mpnl {
 
 // kind 0 = select_kernel (extra = layer), 1 = traverse_kernel, 2 = verify_kernel,
-// 3 = check_kernel, 5 = prep2_kernel (fused prep + top selection)
+// 3 = check_kernel, 5 = prep2_kernel (fused prep + top selection), 6 = soft_llr_kernel
 template <int NN, int L>
 cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp, unsigned grid,
                             int threads, size_t smem, int extra, cudaStream_t st) {
@@ -93,6 +94,12 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
       else if (e == 2) launch(prep2_kernel<NN, L, 2, 4>);
       else launch(prep2_kernel<NN, L, 4, 4>);
     }
+  } else if (kind == 6) {
+    // fp32 list LLRs: CTA = (channel, chunk of vectors), tables staged per CTA
+    auto k = soft_llr_kernel<NN, L>;
+    const int sm = SoftSmem(a.m, NN, L == 2 ? 2 : (L == 4 ? 4 : 6), 4).total_bytes;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    k<<<(unsigned)(a.n_ch * a.soft.chunks), 128, sm, st>>>(a, tp);
   } else if (kind == 2) {
     verify_kernel<NN, L><<<grid, threads, 0, st>>>(a, tp, extra);
   } else {

@@ -631,22 +631,104 @@ def llr_from_candidates(clist: CandidateList, noise_var: float, c: Constellation
 
 
 def mpnl_detect_llrs(plan: BatchPathPlan, h, y, c: Constellation, noise_var=None,
-                     clip: float = LLR_CLIP):
+                     clip: float = LLR_CLIP, *, precision: str = "fp64", return_flags=False):
     """The link simulator's MPNL soft output (linksim.py:151-155):
-    `mpnl_detect_batch` then `_candidate_llrs_batch`, with the candidate list
-    kept on the device between the two kernels.  `noise_var` defaults to the
-    plan's.  Returns LLRs shaped like y's leading axes + (N, log2 Q)."""
+    `mpnl_detect_batch` then `_candidate_llrs_batch`.  `noise_var` defaults to
+    the plan's.  Returns LLRs shaped like y's leading axes + (N, log2 Q).
+
+    precision="fp64" (default): the fp64 full-list kernel, then the list-LLR
+    kernel, the candidate list staying on the device in between — bit-identical
+    to the reference.
+    precision="fp32": the fused fp32 traversal + LLR kernel
+    (`mpnl_detect_llrs_fast`; no candidate list), about 30x faster.  Vectors it
+    flags (an fp32 decision within the guard bound of a boundary on a path that
+    can reach an unclipped LLR) are recomputed by the fp64 path here, so every
+    LLR agrees with the reference within the fp32 metric error,
+    |d llr| <= 2 ped_tol / noise_var (~1e-6 of the metrics / noise_var).  Needs
+    a scalar noise_var; plans without an fp32 path (overloaded channels, more
+    than 3 expanded layers) take the fp64 path.  `return_flags` also returns the
+    boolean mask of recomputed vectors."""
+    if precision not in ("fp64", "fp32"):
+        raise ValueError(f"unknown precision {precision!r}")
     was_np = not isinstance(y, torch.Tensor)
     yt = y if not was_np else torch.from_numpy(np.ascontiguousarray(np.asarray(y))).to(_device())
-    labels, metrics, _ = mpnl_detect_batch(plan, h, yt, c)
-    lead = labels.shape[:-2]
-    n, p = labels.shape[-1], labels.shape[-2]
     nv = plan.noise_var if noise_var is None else noise_var
     if isinstance(nv, np.ndarray) and nv.ndim:
         nv = nv.reshape(-1)
+    fast = (precision == "fp32" and np.ndim(nv) == 0 and not plan.augmented)
+    if fast:
+        out = _detect_llrs_fp32(plan, h, yt, c, float(nv), float(clip))
+        if out is not None:
+            llr, flags = out
+            if was_np:
+                llr, flags = llr.cpu().numpy(), flags.cpu().numpy()
+            return (llr, flags) if return_flags else llr
+    labels, metrics, _ = mpnl_detect_batch(plan, h, yt, c)
+    lead = labels.shape[:-2]
+    n, p = labels.shape[-1], labels.shape[-2]
     llr = _candidate_llrs_batch(labels.reshape(-1, p, n), metrics.reshape(-1, p), nv, c, clip)
     llr = llr.reshape(*lead, n, c.bits_per_symbol)
-    return llr.cpu().numpy() if was_np else llr
+    llr = llr.cpu().numpy() if was_np else llr
+    if return_flags:
+        flags = np.ones(lead, bool) if was_np else torch.ones(lead, dtype=torch.bool,
+                                                               device=llr.device)
+        return llr, flags
+    return llr
+
+
+def _detect_llrs_fp32(plan: BatchPathPlan, h, yt, c: Constellation, nv: float, clip: float):
+    """`mpnl_detect_llrs_fast` + the fp64 re-computation of the vectors it
+    flags.  Returns (llr, recomputed mask) on the device, or None when the plan
+    has no fp32 path."""
+    lib = _lib.load()
+    if c.order != plan.order:
+        raise ValueError("constellation does not match the plan")
+    _check_h(plan, h)
+    yd, y64, _, squeeze = _shape_y(plan, yt)
+    nch, v, m = yd.shape
+    n, bps = plan.n, c.bits_per_symbol
+    dev = yd.device
+    nb = int(lib.mpnl_workspace_bytes(nch * v, n, c.order, plan.expansions.ctypes.data))
+    if nb < 0:
+        return None
+    ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    llr = torch.empty((nch, v, n, bps), dtype=torch.float64, device=dev)
+    flags = torch.empty((nch, v), dtype=torch.uint8, device=dev)
+    rc = lib.mpnl_detect_llrs_fast(plan.perm_dev.data_ptr(), plan.r_dev.data_ptr(),
+                                   plan.qh_dev.data_ptr(), plan.tables.data_ptr(), yd.data_ptr(),
+                                   int(y64), nch, v, m, n, c.order,
+                                   plan.expansions.ctypes.data, plan.noise_var, nv, clip,
+                                   llr.data_ptr(), flags.data_ptr(), ws.data_ptr(), ws.numel(),
+                                   _stream())
+    if rc == _lib.MPNL_EUNSUPPORTED:
+        return None
+    _lib.check(rc, "mpnl_detect_llrs")
+    redo = flags.bool()
+    idx = redo.reshape(-1).nonzero().reshape(-1)
+    if idx.numel():
+        # flagged vectors through the fp64 list path: one plan row per vector
+        ch = idx // v
+        p = plan.n_paths
+        yv = yd.reshape(nch * v, 1, m).index_select(0, idx).contiguous()
+        perm_g = plan.perm_dev.index_select(0, ch).contiguous()
+        r_g = plan.r_dev.index_select(0, ch).contiguous()
+        qh_g = plan.qh_dev.index_select(0, ch).contiguous()
+        k = int(idx.numel())
+        labels = torch.empty((k, p, n), dtype=torch.uint8, device=dev)
+        metrics = torch.empty((k, p), dtype=torch.float64, device=dev)
+        best = torch.empty((k,), dtype=torch.int64, device=dev)
+        rc = lib.mpnl_detect_full(perm_g.data_ptr(), r_g.data_ptr(), qh_g.data_ptr(),
+                                  yv.data_ptr(), int(y64), k, 1, m, n, c.order,
+                                  plan.expansions.ctypes.data, plan.noise_var,
+                                  labels.data_ptr(), metrics.data_ptr(), best.data_ptr(), _stream())
+        _lib.check(rc, "mpnl_detect_llrs (fp64 recomputation)")
+        fix = _candidate_llrs_batch(labels, metrics, nv, c, clip)
+        llr.reshape(nch * v, n, bps).index_copy_(0, idx, fix)
+    if squeeze == "batch":
+        llr, redo = llr[:, 0], redo[:, 0]
+    elif squeeze == "vec":
+        llr, redo = llr[0, 0], redo[0, 0]
+    return llr, redo
 
 
 def mpnl_detect(plan: PathPlan, inp: DetectorInput):
