@@ -215,7 +215,7 @@ def _frame_rng(seed: int, chan_idx: int, frame_idx: int):
     return np.random.default_rng(np.random.SeedSequence(entropy=(seed, chan_idx, frame_idx)))
 
 
-def _detect_llrs(cfg, c, h_flat, y_rc, noise_var, plan=None):
+def _detect_llrs(cfg, c, h_flat, y_rc, noise_var, plan=None, precision="fp64"):
     """LLRs (n_re, V, N, bps) of y_rc (n_re, V, M) against the n_re per-RE
     channels h_flat (linksim.py:140-156, the V frames batched per channel)."""
     if cfg.detector in ("zf", "mmse"):
@@ -226,14 +226,18 @@ def _detect_llrs(cfg, c, h_flat, y_rc, noise_var, plan=None):
         return llr.reshape(n_re, v, h_flat.shape[2], c.bits_per_symbol)
     if plan is None:
         plan = _det.mpnl_plan_batch(h_flat, noise_var, cfg.n_paths, c)
-    return _det.mpnl_detect_llrs(plan, h_flat, y_rc, c, noise_var)
+    return _det.mpnl_detect_llrs(plan, h_flat, y_rc, c, noise_var, precision=precision)
 
 
-def simulate_frames(cfg, grid, noise_var: float, chan_idx: int, frame_indices) -> np.ndarray:
+def simulate_frames(cfg, grid, noise_var: float, chan_idx: int, frame_indices, *,
+                    soft_precision: str = "fp64") -> np.ndarray:
     """Frames on one channel realisation (linksim.py:159-232): boolean
     (n_frames, n_streams), True = transport block decoded correctly.
     `grid` has `.h` (symbols, subcarriers, >= M, >= N) (the reference's
-    ChannelGrid) or is that array."""
+    ChannelGrid) or is that array.  `soft_precision` selects the MPNL soft
+    output: "fp64" (the reference's arithmetic; outcomes identical to the
+    reference's) or "fp32" (`detect.mpnl_detect_llrs(precision="fp32")`: LLRs
+    within ~1e-6 of the metrics / noise_var of the reference's)."""
     num = cfg.numerology
     n_sc = cfg.n_subcarriers
     n, m = cfg.n_streams, cfg.m_antennas
@@ -277,7 +281,8 @@ def simulate_frames(cfg, grid, noise_var: float, chan_idx: int, frame_indices) -
     y = receive_grid(h, x, noise_d)                                       # (f, s, sc, m)
     if cfg.csi == "genie":
         h_flat, y_flat = data_re_batch(h, y, data_syms)                  # (n_re,m,n), (f,n_re,m)
-        llrs = _detect_llrs(cfg, c, h_flat, y_flat.permute(1, 0, 2).contiguous(), noise_var)
+        llrs = _detect_llrs(cfg, c, h_flat, y_flat.permute(1, 0, 2).contiguous(), noise_var,
+                            precision=soft_precision)
         llrs = llrs.permute(1, 0, 2, 3)                                   # (f, n_re, n, bps)
     else:
         llrs = torch.empty((f, n_re, n, bps), dtype=torch.float64, device=dev)
@@ -286,7 +291,7 @@ def simulate_frames(cfg, grid, noise_var: float, chan_idx: int, frame_indices) -
             h_est = estimate_channel_ls(y[i], pil, cfg)
             h_flat, y_flat = data_re_batch(h_est, y[i:i + 1], data_syms)
             llrs[i] = _detect_llrs(cfg, c, h_flat, y_flat.permute(1, 0, 2).contiguous(),
-                                   noise_var)[:, 0]
+                                   noise_var, precision=soft_precision)[:, 0]
     # per-vehicle LLR concatenation in RE order -> rate-matched LDPC decoding
     llrs_v = llrs.permute(0, 2, 1, 3).reshape(f * n, n_re * bps).contiguous()
     dec, conv = _fec.decode_rate_matched(code, rm, llrs_v)

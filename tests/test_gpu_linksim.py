@@ -31,6 +31,22 @@ def test_simulate_frames_matches_reference(case):
     assert np.array_equal(ok, GOLD[name]), f"{name}: {int((ok != GOLD[name]).sum())} outcomes differ"
 
 
+@pytest.mark.parametrize("case", [c for c in lc.CASES if c[5] == "mpnl"],
+                         ids=[c[0] for c in lc.CASES if c[5] == "mpnl"])
+def test_simulate_frames_fp32_soft_output(case):
+    """The fp32 soft output (fused traversal + LLR kernel) perturbs LLRs by
+    ~1e-6 of the metrics / noise_var: on these seeded cases every decode outcome
+    still equals the reference's."""
+    from paper_2409_14355_b200 import linksim as L
+    name, n, m, (q, rn, rd), rb, det, csi, p, snr, f = case
+    mcs = SimpleNamespace(constellation=constellation_for(q), code_rate=Fraction(rn, rd))
+    cfg = L.LinkConfig(n_streams=n, m_antennas=m, mcs=mcs, rb_per_vehicle=rb, detector=det,
+                       n_paths=p, csi=csi)
+    ok = L.simulate_frames(cfg, lc.channel(case), lc.noise_var(case), 3, range(f),
+                           soft_precision="fp32")
+    assert np.array_equal(ok, GOLD[name]), f"{name}: {int((ok != GOLD[name]).sum())} outcomes differ"
+
+
 def test_config_validation_like_reference():
     from paper_2409_14355_b200 import linksim as L
     mcs = SimpleNamespace(constellation=constellation_for(4), code_rate=Fraction(1, 2))

@@ -40,6 +40,16 @@ gpu_s = (time.perf_counter() - t0) / reps
 line = {"what": "simulate_frames (one channel, a batch of frames), wall clock incl. host RNG",
         "config": f"{n}x{m} 16-QAM r={rate}, {rb} RB, detector {det} P=32, genie CSI, {f} frames",
         "gpu_frames_per_s": round(f / gpu_s, 1), "gpu_ms_per_batch": round(gpu_s * 1e3, 2)}
+if det == "mpnl":   # the fp32 soft output (fused traversal + LLR kernel)
+    for _ in range(2):
+        L.simulate_frames(cfg, h, nv, 0, range(f), soft_precision="fp32")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for r in range(reps):
+        ok32 = L.simulate_frames(cfg, h, nv, 0, range(r * f, (r + 1) * f), soft_precision="fp32")
+    s32 = (time.perf_counter() - t0) / reps
+    line["gpu_fp32_soft_frames_per_s"] = round(f / s32, 1)
+    line["fp32_soft_outcomes_equal_fp64"] = bool(np.array_equal(ok32, ok))
 try:
     sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
     sys.dont_write_bytecode = True
