@@ -364,8 +364,10 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     const int nvi = (bpv > 1 || vpi == 1) ? 1 : vpi;
     const int64_t items = n_ch * ((v_per_ch + nvi - 1) / nvi);
     if (items > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "too many work items");
+    // channels with fewer than two path batches per warp: a warp per channel
+    a.wpc = ((v_per_ch + nvi - 1) / nvi) * (int64_t)bpv < 2 * warps && n_ch >= 2 * warps ? 1 : 0;
     if (stage == 2) {
-      const TravSmem so(m, n, warps, nvi, tp.list_bytes);
+      const TravSmem so(m, n, warps, nvi, tp.list_bytes, a.wpc != 0);
       e = launch_fast(n, L, 1, a, tp, 0, threads, so.total_bytes, (int)items, st);
       if (e != cudaSuccess) return cuda_fail(e, "traverse kernel");
     } else {

@@ -76,6 +76,7 @@ struct DetectArgs {
   int vpi, bpv;             // vectors per warp item (VPI mode) / path batches per vector
   int metric_offset;        // 1 when M > N: add ||y||^2 - ||z||^2
   float guard_scale;        // scales the fp32 error bound (1 = rigorous)
+  int wpc;                  // traversal: 1 = a warp per channel (few vectors per channel)
   SoftArgs soft;            // soft_llr_kernel only
 };
 
@@ -1093,7 +1094,8 @@ struct TravSmem {
   int tpo, tab, wbuf, bufsz, zs, thr, lst, eac, mbar, xs, ev, evn, total_bytes;   // floats / bytes
   int ck, cv;   // items and vectors per chunk
   int tab0, tabn;   // staged slice of the channel's table blob (per-layer float4 + r'' columns)
-  __host__ __device__ TravSmem(int m, int n, int warps, int nvi, int list_bytes) {
+  // wpc: warp-per-channel mode, every warp stages its own channel's table slice
+  __host__ __device__ TravSmem(int m, int n, int warps, int nvi, int list_bytes, bool wpc = false) {
     TableLayout tl(m, n);
     const int npp = (n + 1) / 2, n4 = (n + 3) & ~3;
     // chunk: up to MPNL_CHUNK_V vectors, at most ~2 KB per buffer (large
@@ -1112,9 +1114,12 @@ struct TravSmem {
     bufsz = eac + TableLayout::up4(2 * (cv + 2));
     int o = 0;
     tpo = o; o += TableLayout::up4((int)(sizeof(TreeParams) / 4));
-    tab0 = tl.off_lay;                             // Q^H and the shift are not read here
-    tabn = tl.total - tl.off_lay;
-    tab = o; o += tabn;
+    // Q^H and the shift are not read here: wide channels (whose fp64 Q^H is the
+    // bulk of the blob) stage only the per-layer and r'' blocks; small ones keep
+    // the whole blob (measured: C2 traversal 300 vs 306 us with the slice)
+    tab0 = n > 16 ? tl.off_lay : 0;
+    tabn = tl.total - tab0;
+    tab = o; o += (wpc ? warps : 1) * tabn;
     wbuf = o; o += warps * 2 * bufsz;
     mbar = o; o += warps * 2 * 2;                  // u64 mbarrier per warp buffer
     xs = o; o += 2 * MPNL_XMAX * MPNL_PT_SMALL * MPNL_XS_STRIDE;   // u64 per-thread symbols
@@ -1182,12 +1187,18 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   extern __shared__ __align__(16) float sm[];
   const int nth = blockDim.x, nw = nth >> 5;
   const int nvi = VPI ? a.vpi : 1;                          // vectors per item
-  const TravSmem so(a.m, N, nw, nvi, tparam.list_bytes);
+  // Warp-per-channel mode (a.wpc; channels with only a few vectors, e.g. one H
+  // per vector as in the reference's own bench, cli.py:227-239): every warp
+  // walks whole channels with its own table slot and no block barrier, instead
+  // of the CTA staging one channel and splitting its vectors over the warps.
+  const bool wpc = a.wpc != 0;
+  const TravSmem so(a.m, N, nw, nvi, tparam.list_bytes, wpc);
   const TableLayout tl(a.m, N);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const float INF = __int_as_float(0x7f800000);
   TreeParams& tp = *reinterpret_cast<TreeParams*>(sm + so.tpo);
-  float* tab = sm + so.tab - so.tab0;   // virtual blob base: only [tab0, total) is staged
+  float* tabs = sm + so.tab + (wpc ? warp * so.tabn : 0);   // staged slice [tab0, total)
+  float* tab = tabs - so.tab0;                               // virtual blob base
   float* wb0 = sm + so.wbuf + warp * 2 * so.bufsz;
   uint64_t* wbar = reinterpret_cast<uint64_t*>(sm + so.mbar) + 2 * warp;
   if (lane == 0) {
@@ -1253,15 +1264,20 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     if (slot) __nanosleep((unsigned)(slot * MPNL_SKEW_NS));
   }
 #endif
-  for (int seg = it_begin; seg < it_end;) {
+  if (wpc) __syncthreads();   // xs / tp ready (the CTA mode's first segment barrier does it)
+  const int64_t wstep = (int64_t)gridDim.x * nw * ipc;   // wpc: this warp's channel stride, in items
+  const int64_t wseg0 = ((int64_t)blockIdx.x * nw + warp) * ipc;
+  const int seg_stop = wpc ? (int)I : it_end;
+  for (int seg = wpc ? (int)min(wseg0, I) : it_begin; seg < seg_stop;) {
     const int c = seg / ipc;
     const int ibase = c * ipc, vbase = c * V;
-    const int seg_end = min(it_end, ibase + ipc);
-    // warp w owns the balanced item range [wb, we) of the segment, walked in
-    // chunks of so.ck items (contiguous vectors, one bulk-copy group each); the
-    // first chunk's copies are issued before the table staging (they overlap)
-    const int wb = seg + (int)((int64_t)warp * (seg_end - seg) / nw);
-    const int we = seg + (int)((int64_t)(warp + 1) * (seg_end - seg) / nw);
+    const int seg_end = wpc ? ibase + ipc : min(it_end, ibase + ipc);
+    // warp w owns the balanced item range [wb, we) of the segment (the whole
+    // channel in wpc mode), walked in chunks of so.ck items (contiguous vectors,
+    // one bulk-copy group each); the first chunk's copies are issued before the
+    // table staging (they overlap)
+    const int wb = wpc ? seg : seg + (int)((int64_t)warp * (seg_end - seg) / nw);
+    const int we = wpc ? seg_end : seg + (int)((int64_t)(warp + 1) * (seg_end - seg) / nw);
     const int nchunk = (we - wb + so.ck - 1) / so.ck;
     int k = 0;
     int ch = 0;
@@ -1271,13 +1287,14 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
       trav_issue<N>(a, so, wb0, wbar, vbase + (i0 - ibase) * nvi,
                     min((i1 - ibase) * nvi, V) - (i0 - ibase) * nvi, lbytes);
     }
-    __syncthreads();   // previous segment's tables no longer in use (and xs / tp ready)
+    // previous segment's tables no longer in use (and xs / tp ready)
+    if (wpc) __syncwarp(); else __syncthreads();
     {
       const float4* src = reinterpret_cast<const float4*>(a.tables + (int64_t)c * tl.total + so.tab0);
-      float4* dst = reinterpret_cast<float4*>(sm + so.tab);
-      for (int i = tid; i < so.tabn / 4; i += nth) dst[i] = src[i];
+      float4* dst = reinterpret_cast<float4*>(tabs);
+      for (int i = wpc ? lane : tid; i < so.tabn / 4; i += wpc ? 32 : nth) dst[i] = src[i];
     }
-    __syncthreads();
+    if (wpc) __syncwarp(); else __syncthreads();
     for (; ch < nchunk; ++ch, k ^= 1) {
       if (ch + 1 < nchunk && lane == 0) {
         const int i0 = wb + (ch + 1) * so.ck;
@@ -1438,7 +1455,12 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     }
       __syncwarp();   // the chunk buffer is refilled by the next issue into it
     }
-    seg = seg_end;
+    if (wpc) {
+      const int64_t nx = (int64_t)seg + wstep;
+      seg = nx < (int64_t)seg_stop ? (int)nx : seg_stop;
+    } else {
+      seg = seg_end;
+    }
   }
   // ---- flush the CTA's event buffer to the global log ----
   __syncthreads();

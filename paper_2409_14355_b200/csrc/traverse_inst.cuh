@@ -71,6 +71,8 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
       int waves = work >= 64LL * cap * (threads / 32) ? MPNL_TRAV_WAVES : 1;
       if (env_waves > 0) waves = env_waves;
       grid = (unsigned)std::min<long long>(cap * waves, (long long)extra);
+      if (a.wpc)   // a warp per channel: one wave of CTAs, never more warps than channels
+        grid = (unsigned)std::min<long long>(cap, (a.n_ch + threads / 32 - 1) / (threads / 32));
     }
     k<<<grid, threads, smem, st>>>(a, tp);
   } else if (kind == 5) {

@@ -55,6 +55,34 @@ def test_plan_matches_reference(name):
     np.testing.assert_allclose(plan.qh, g[f"{name}_qh"], rtol=0, atol=1e-11)
 
 
+@pytest.mark.parametrize("m,n,dt", [(8, 8, np.complex64), (16, 8, np.complex64), (24, 5, np.complex128),
+                                    (32, 8, np.complex64), (12, 12, np.complex128),
+                                    (24, 16, np.complex64), (32, 12, np.complex64),
+                                    (24, 24, np.complex64), (32, 24, np.complex128),
+                                    (32, 32, np.complex64), (31, 17, np.complex64),
+                                    (40, 24, np.complex64), (64, 32, np.complex64),
+                                    (3, 5, np.complex64), (20, 12, np.complex64),
+                                    (12, 20, np.complex128), (24, 28, np.complex64),
+                                    (1, 1, np.complex64), (7, 1, np.complex64)])
+def test_plan_shapes_vs_oracle(m, n, dt):
+    """Every plan-kernel instance (row-count bucket x lane-group width of the
+    register kernel, the shared-memory CTA kernel beyond 32 rows; plain and
+    augmented channels; both input types) against the oracle's sorted QR
+    (itself pinned to the reference): same permutation, R and Q^H to 1e-11."""
+    det = _det()
+    rng = np.random.default_rng(1000 * m + n)
+    nch = 37
+    h = ((rng.standard_normal((nch, m, n)) + 1j * rng.standard_normal((nch, m, n)))
+         / np.sqrt(2)).astype(dt)
+    order = 16
+    plan = det.mpnl_plan_batch(h, 0.2, 8, constellation_for(order))
+    ref = orc.plan_channels(h, 0.2, 8, order)
+    assert plan.augmented == (n > m)
+    assert np.array_equal(plan.perm, ref.perm)
+    np.testing.assert_allclose(plan.r, ref.r, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(plan.qh, ref.qh, rtol=0, atol=1e-11)
+
+
 def test_plan_overloaded_matches_reference():
     det = _det()
     g = np.load(GOLD / "plan.npz")

@@ -1,5 +1,5 @@
 """One plan + hard detection of a config (for ncu captures).
-usage: python tools/profile_one.py C2 [n_rb] [reps]"""
+usage: python tools/profile_one.py C2 [n_rb] [reps] [soft]   (soft: also the fp32 soft output)"""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -25,6 +25,8 @@ ws = torch.empty(int(lib.mpnl_workspace_bytes(y.shape[0] * y.shape[1], cfg.n, cf
 for _ in range(reps):
     plan = det.mpnl_plan_batch(h, float(d["nv"][0]), cfg.n_paths, c)
     hard, metric, flags = det.mpnl_detect_hard(plan, h, y, c, return_flags=True, workspace=ws)
+if len(sys.argv) > 4 and sys.argv[4] == "soft":
+    det.mpnl_detect_llrs(plan, h, y[:, :168].contiguous(), c, precision="fp32")
 torch.cuda.synchronize()
 nv_ = y.shape[0] * y.shape[1]
 st = det.workspace_stats(ws)

@@ -1,5 +1,13 @@
-import sys, numpy as np, torch
-sys.path.insert(0, '/root/repo')
+"""Device time of the fp32 soft-output call (prep + fused traversal/LLR kernel,
+C-ABI mpnl_detect_llrs_fast; CUDA events over 10 calls) and its flagged fraction.
+
+    python tools/soft_time.py CFG n_rb"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
 from paper_2409_14355_b200 import detect as det, _lib
 from paper_2409_14355_b200.core import constellation_for, LLR_CLIP
 from paper_2409_14355_b200.workloads import CONFIGS, generate
