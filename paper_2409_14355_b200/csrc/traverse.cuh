@@ -1179,7 +1179,7 @@ __device__ __forceinline__ void trav_issue(const DetectArgs& a, const TravSmem& 
 // ONEB: (SH, P == 32 PT) every vector is exactly one full batch: the path
 // bookkeeping is compile-time (loop-invariant) and the lane's two paths are
 // ordered with one compare instead of running top-3 inserts.
-template <int N, int L, bool VPI, bool SH = false, bool ONEB = false>
+template <int N, int L, bool VPI, bool SH = false, bool ONEB = false, bool WPC = false>
 __global__ void __launch_bounds__(TravCfg<N>::MAXT, TravCfg<N>::MINB)
 traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   constexpr int PT = TravCfg<N>::PT;
@@ -1191,7 +1191,9 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   // per vector as in the reference's own bench, cli.py:227-239): every warp
   // walks whole channels with its own table slot and no block barrier, instead
   // of the CTA staging one channel and splitting its vectors over the warps.
-  const bool wpc = a.wpc != 0;
+  // (a template parameter: the CTA-mode instances keep their instruction schedule)
+  constexpr bool wpc = WPC;
+  static_assert(!WPC || (!SH && !ONEB), "warp-per-channel mode: plain or VPI instances");
   const TravSmem so(a.m, N, nw, nvi, tparam.list_bytes, wpc);
   const TableLayout tl(a.m, N);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

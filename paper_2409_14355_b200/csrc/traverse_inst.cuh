@@ -50,6 +50,9 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
                        : (oneb ? traverse_kernel<NN, L, false, CAN_SH, CAN_SH>
                                : (sh ? traverse_kernel<NN, L, false, CAN_SH>
                                      : traverse_kernel<NN, L, false>));
+    if (a.wpc)   // a warp per channel (few vectors per channel): plain or VPI instance
+      k = a.vpi > 1 ? traverse_kernel<NN, L, true, false, false, true>
+                    : traverse_kernel<NN, L, false, false, false, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (grid == 0) {
       int nb = 0, dev = 0, sms = 148;

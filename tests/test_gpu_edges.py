@@ -52,6 +52,24 @@ def test_shapes_vs_oracle(m, n, order, p):
     _check(h, y, nv, p, c, hard, metric)
 
 
+@pytest.mark.parametrize("n_ch,v,m,n,order,p", [(300, 1, 8, 8, 16, 32), (257, 3, 12, 12, 16, 64),
+                                                (70, 2, 24, 24, 64, 64), (40, 1, 32, 32, 16, 32),
+                                                (9, 1, 8, 8, 16, 32), (130, 5, 16, 16, 64, 16)])
+def test_few_vectors_per_channel(n_ch, v, m, n, order, p):
+    """One H per vector (the reference's own bench shape, cli.py:227-239) and
+    other channels with only a few vectors: the traversal's warp-per-channel
+    mode (every warp stages its own channel's tables), against the oracle."""
+    det = _det()
+    rng = np.random.default_rng(n_ch * 100 + v)
+    c, h, y, nv = _case(rng, n_ch, v, m, n, order, snr_db=16.0)
+    plan = det.mpnl_plan_batch(h, nv, p, c)
+    hard, metric = det.mpnl_detect_hard(plan, h, y, c)
+    _check(h, y, nv, p, c, hard, metric)
+    llr = det.mpnl_detect_llrs(plan, h, y, c, precision="fp32")
+    ref = det.mpnl_detect_llrs(plan, h, y, c)
+    assert np.abs(llr - ref).max() <= 1e-3
+
+
 def test_empty_and_ragged_batches():
     import torch
     det = _det()
