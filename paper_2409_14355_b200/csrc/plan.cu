@@ -10,12 +10,17 @@
 //   * r_kk recomputed from the pivot column, floored at 1e-300 (348-350);
 //   * Q^H = top M rows of Q, conjugate-transposed (383).
 //
-// B200 mapping: one 4-warp CTA per channel.  Lane j owns *physical* column j
-// of A in shared memory (A[m][j], padded rows); the column bookkeeping (norms,
-// logical positions) is replicated identically in every warp, so column swaps
-// are pure bookkeeping and no data moves.  Each warp owns a quarter of the
-// rows for the projections and updates (partials summed in a fixed order);
-// r_kk is a block reduction over rows.
+// B200 mapping: channels of up to 32 rows (every BASELINE config) take
+// `plan_qr_reg_kernel`: a lane group of 8 / 16 / 32 lanes per channel, lane j
+// holding column j of A in registers, no block barriers (see the kernel's
+// comment).  Taller channels (m, or m + n when augmented, above 32) take
+// `plan_qr_kernel`: one 4-warp CTA per channel, lane j owning *physical* column
+// j of A in shared memory (A[m][j], padded rows), the column bookkeeping
+// (norms, logical positions) replicated identically in every warp so that
+// column swaps are pure bookkeeping, each warp owning a quarter of the rows for
+// the projections and updates (partials summed in a fixed order), r_kk a block
+// reduction over rows.  One kernel per shape, whatever the number of channels:
+// plans never depend on the batch size.
 // Everything is fp64; the fast path's fp32 tables are derived at the end.
 #include "common.cuh"
 
@@ -280,7 +285,7 @@ plan_qr_kernel(const TIn* __restrict__ h, int64_t n_ch, int m, int n, int L,
 // reading q as shared-memory broadcasts.  R is kept by physical column in
 // shared memory and put in logical order at the end.  Against the CTA kernel
 // (one block barrier chain per column, A in shared memory): C5's 2,048
-// 24 x 24 channels 131 -> see DESIGN §4.
+// 24 x 24 channels 131 -> 90 us, 8,192 8 x 8 channels 66 -> 25 us.
 // ---------------------------------------------------------------------------
 template <int G>
 __device__ __forceinline__ double group_sum_d(double v) {
@@ -454,7 +459,6 @@ static cudaError_t launch_plan_reg(const TIn* h, int64_t n_ch, int m, int n, int
                                    int augmented, int32_t* perm, double2* r64, double2* qh64,
                                    float* tables, cudaStream_t st) {
   constexpr int WARPS = 2, GPC = WARPS * (32 / G);   // groups (channels) per CTA
-  const int ma = augmented ? m + n : m;
   const size_t smem = (size_t)GPC * PlanRegSmem(n).total * sizeof(double2);
   auto k = plan_qr_reg_kernel<MA, G, TIn>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
