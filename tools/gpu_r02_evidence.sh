@@ -18,7 +18,7 @@ python tools/soft_bench.py C5P64 64 1 > gpurun_out/e_soft_C5P64.json 2>/dev/null
 python tools/soft_time.py C2 273 > gpurun_out/e_soft_kernel_times.txt 2>/dev/null
 for a in "C3 273" "C4 64" "C5P64 64" "C5P256 32" "C5P1024 16"; do python tools/soft_time.py $a >> gpurun_out/e_soft_kernel_times.txt 2>/dev/null; done
 (python tools/linksim_bench.py 25 mpnl; python tools/linksim_bench.py 100 mpnl; python tools/linksim_bench.py 25 mmse) > gpurun_out/e_linksim_bench.jsonl 2>/dev/null
-./tools/probes/ffma2_forms > gpurun_out/e_ffma2_forms.txt 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/ffma2_forms tools/probes/ffma2_forms.cu && /tmp/ffma2_forms > gpurun_out/e_ffma2_forms.txt 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/e_launches_default.csv \
     python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu-baseline > /dev/null 2>&1; echo launches rc=$?
 bash tools/prof_full.sh e_ncu_traverse_C5P1024 C5P1024 traverse_kernel
