@@ -86,7 +86,7 @@ struct DetectArgs {
 #define MPNL_U 5.9604645e-08f   // 2^-24
 #define EV_NODE 0   // (a NODE event's .w carries -evp: negative, see ev_node_w)
 #define EV_CUT 1
-#define TRAV_EV_CAP 256         // per-CTA event buffer of the traversal kernel
+#define TRAV_EV_CAP 512         // per-CTA event buffer of the traversal kernel
 #define MPNL_XS_STRIDE 128      // = traversal threads per CTA (per-thread symbol slots)
 
 // ---------------------------------------------------------------------------
@@ -234,6 +234,13 @@ __device__ __forceinline__ float sqrt_up(float b) {
 __device__ __forceinline__ float ped_tol(float b, float eacc, int n) {
   return __fadd_ru(__fadd_ru(__fmul_ru(__fmul_ru(2.f, sqrt_up(b)), eacc), __fmul_ru(eacc, eacc)),
                    __fmul_ru(2.f * n * MPNL_U, b));
+}
+
+// a vector's final event bound: a marked decision whose PED prefix exceeds it cannot
+// affect the result.  One explicit instruction sequence, because the traversal's
+// flush and the check kernel must agree on it exactly.
+__device__ __forceinline__ float node_lim(float4 res, int n) {
+  return __fmaf_rn(2.f, ped_tol(res.x, res.w, n), res.x);
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -651,23 +658,61 @@ __device__ __forceinline__ void select_nearest(float xl, float yl, int E, int th
       j += tb ? 1 : 0;
       ct = ct || (!ta && !tb);
     }
+  } else if constexpr (L == 8) {
+    // 64-QAM, E > 4.  Row i of the merge (the x-axis order's i-th level) offers the sum
+    // dx_i + dy_{w_i}; its KEY is that sum with the three low mantissa bits replaced by
+    // i, so the frontier's minimum and its row come out of one min tree (FMNMX3) and a
+    // mask instead of a compare/select chain.  Keys, per-axis orders and column counters
+    // live in per-thread (transposed) shared memory, so every data-dependent access is
+    // one LDS / STS.  Keys are non-decreasing along a row, hence the picks are exactly
+    // the E smallest cells in KEY order; that order differs from the exact one only
+    // between sums closer than 8 ulp, and the returned kprev / knext are keys (within
+    // 8 ulp below the sums): select_cut_slack() widens the cut guard accordingly, so a
+    // cut that the truncation could have changed is always logged and re-selected in
+    // fp64 by the check kernel.
+    __shared__ float sdx[L][128], sdy[L][128];
+    __shared__ float4 snk[2][128];
+    __shared__ uint8_t sox[L][128], soy[L][128], sw[L][128];
+    const float BIG = 1e30f;
+    auto mkkey = [](float v, unsigned row) {
+      return __uint_as_float((__float_as_uint(v) & ~7u) | row);
+    };
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      sdx[i][th] = dx[i]; sdy[i][th] = dy[i];
+      sox[i][th] = (uint8_t)ox[i]; soy[i][th] = (uint8_t)oy[i]; sw[i][th] = 0;
+    }
+    snk[0][th] = make_float4(mkkey(dx[0] + dy[0], 0u), mkkey(dx[1] + dy[0], 1u),
+                             mkkey(dx[2] + dy[0], 2u), mkkey(dx[3] + dy[0], 3u));
+    snk[1][th] = make_float4(mkkey(dx[4] + dy[0], 4u), mkkey(dx[5] + dy[0], 5u),
+                             mkkey(dx[6] + dy[0], 6u), mkkey(dx[7] + dy[0], 7u));
+    float* nkf = reinterpret_cast<float*>(&snk[0][th]);
+#pragma unroll
+    for (int pick = 0; pick <= EMAX; ++pick) {
+      if (pick > E) break;
+      const float4 ka = snk[0][th], kb = snk[1][th];
+      const float best = fminf(fminf(fminf(fminf(ka.x, ka.y), ka.z), fminf(fminf(ka.w, kb.x), kb.y)),
+                               fminf(kb.z, kb.w));
+      if (pick < E) {
+        const int sel = (int)(__float_as_uint(best) & 7u);
+        const int col = sw[sel][th];
+        const unsigned b = ((unsigned)sox[sel][th] << 3) | (unsigned)soy[col][th];
+        const int cn = col + 1 < L ? col + 1 : L - 1;
+        const float nxt = (col + 1 < L) ? sdx[sel][th] + sdy[cn][th] : BIG;
+        nkf[(sel >> 2) * (128 * 4) + (sel & 3)] = mkkey(nxt, (unsigned)sel);
+        sw[sel][th] = (uint8_t)(col + 1);
+        words[pick >> 2] |= b << (8 * (pick & 3));
+        kprev = best;
+      } else {
+        knext = best;
+      }
+    }
   } else {
+    // L <= 4: a register-resident merge (the orders are short select chains)
     int w[L];
     float nk[L];
 #pragma unroll
     for (int i = 0; i < L; ++i) { w[i] = 0; nk[i] = dx[i] + dy[0]; }
-    // L = 8: the per-axis orders live in per-thread (transposed) shared memory,
-    // so the merge's data-dependent lookups are single LDS instead of select chains
-    constexpr bool SMEM = L == 8;
-    __shared__ float sdx[SMEM ? L : 1][128], sdy[SMEM ? L : 1][128];
-    __shared__ uint8_t sox[SMEM ? L : 1][128], soy[SMEM ? L : 1][128], sw[SMEM ? L : 1][128];
-    if (SMEM) {
-#pragma unroll
-      for (int i = 0; i < L; ++i) {
-        sdx[i][th] = dx[i]; sdy[i][th] = dy[i];
-        sox[i][th] = (uint8_t)ox[i]; soy[i][th] = (uint8_t)oy[i]; sw[i][th] = 0;
-      }
-    }
 #pragma unroll
     for (int pick = 0; pick <= EMAX; ++pick) {
       if (pick > E) break;
@@ -680,24 +725,14 @@ __device__ __forceinline__ void select_nearest(float xl, float yl, int E, int th
         sel = lt ? i : sel;
       }
       if (pick < E) {
-        int col;
-        unsigned b;
-        float nxt;
-        if (SMEM) {
-          col = sw[sel][th];
-          b = ((unsigned)sox[sel][th] << 3) | (unsigned)soy[col][th];
-          nxt = (col + 1 < L) ? sdx[sel][th] + sdy[col + 1][th] : INF;
-          sw[sel][th] = (uint8_t)(col + 1);
-        } else {
-          col = dyn_at(w, sel);
-          b = (unsigned)((dyn_at(ox, sel) << 3) | dyn_at(oy, col));
-          nxt = (col + 1 < L) ? dyn_at(dx, sel) + dyn_at(dy, col + 1) : INF;
-        }
+        const int col = dyn_at(w, sel);
+        const unsigned b = (unsigned)((dyn_at(ox, sel) << 3) | dyn_at(oy, col));
+        const float nxt = (col + 1 < L) ? dyn_at(dx, sel) + dyn_at(dy, col + 1) : INF;
         words[pick >> 2] |= b << (8 * (pick & 3));
         kprev = best;
 #pragma unroll
         for (int i = 0; i < L; ++i)
-          if (i == sel) { if (!SMEM) w[i] = col + 1; nk[i] = nxt; }
+          if (i == sel) { w[i] = col + 1; nk[i] = nxt; }
       } else {
         knext = best;
       }
@@ -851,11 +886,18 @@ __device__ __forceinline__ void store_selection(uint8_t* out, int E,
   }
 }
 
-// cut guard: distance keys are within 2 sqrt2 E (sqrt k) + 2E^2 (+ rounding)
-__device__ __forceinline__ bool cut_near(float kprev, float knext, float Eb) {
+// cut guard: distance keys are within 2 sqrt2 E (sqrt k) + 2E^2 (+ rounding).
+// slack_u: extra relative slack in units of u = 2^-24 (select_cut_slack: the key-ordered
+// 64-QAM merge returns sums truncated by up to 8 ulp = 16 u each and may order sums
+// closer than that either way).
+__device__ __forceinline__ bool cut_near(float kprev, float knext, float Eb, float slack_u = 0.f) {
   const float bound = 2.8284272f * Eb * (sqrt_up(kprev) + sqrt_up(knext)) + 4.f * Eb * Eb +
-                      8.f * MPNL_U * (knext + 1.f);
+                      (8.f + slack_u) * MPNL_U * (fmaxf(knext, kprev) + 1.f);
   return knext - kprev <= bound;
+}
+template <int L, int EMAX>
+__device__ __forceinline__ constexpr float select_cut_slack() {
+  return (L == 8 && EMAX > 4) ? 64.f : 0.f;
 }
 
 template <int N, int L, int EMAX>
@@ -894,7 +936,8 @@ select_kernel(const DetectArgs a, const TreeParams tp, int pos, int npar, int vb
   select_nearest<L, EMAX>(__fmul_rn(xr, kx), __fmul_rn(xi, kx), E,
                           threadIdx.y * blockDim.x + threadIdx.x, words, kprev, knext);
   store_selection<EMAX>(vlist + tp.list_off[pos] + par * E, E, words);
-  if (cut_near(kprev, knext, 0.5f - thr_pos)) log_event(a, make_int4(p0, pos, (int)gv, EV_CUT));
+  if (cut_near(kprev, knext, 0.5f - thr_pos, select_cut_slack<L, EMAX>()))
+    log_event(a, make_int4(p0, pos, (int)gv, EV_CUT));
 }
 
 // ===========================================================================
@@ -1215,7 +1258,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     const int* s = reinterpret_cast<const int*>(&tparam);
     int* d = reinterpret_cast<int*>(&tp);
     for (int i = tid; i < (int)(sizeof(TreeParams) / 4); i += nth) d[i] = s[i];
-    if (tid == 0) { evn[0] = 0; evn[1] = 0; }
+    if (tid == 0) { evn[0] = 0; evn[1] = 0; evn[2] = 0; evn[3] = 0; }
   }
   const int P = tparam.n_paths;
   const int lbytes = tparam.list_bytes;
@@ -1465,17 +1508,50 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
     }
   }
   // ---- flush the CTA's event buffer to the global log ----
+  // A NODE event was logged against the vector's RUNNING best; every vector of
+  // this CTA is finished now, so the event is first tested against the FINAL
+  // bound -- the very test check_kernel applies before doing any work
+  // (node_lim) -- and only the survivors reach the global log (C5/P1024: 2.0 ->
+  // 0.8 events per vector).
   __syncthreads();
   const int n_ev = min(evn[0], TRAV_EV_CAP);
+  for (int i0 = 0; i0 < n_ev; i0 += nth) {
+    const int i = i0 + tid;
+    bool keep = i < n_ev;
+    if (keep) {
+      const int4 e = evb[i];
+      if (ev_is_node(e.w)) {
+        keep = ev_node_evp(e.w) <= node_lim(__ldcg(a.vres + (unsigned)e.z), N);
+        if (!keep) evb[i].y = 0;   // a logged NODE event always has a non-zero mask
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0 && bal) atomicAdd(evn + 2, __popc(bal));
+  }
+  __syncthreads();
+  const int n_keep = evn[2];
   if (tid == 0) {
-    evn[1] = n_ev ? atomicAdd(a.counters + 1, n_ev) : 0;
-    if (a.stats && n_ev) atomicAdd(a.stats, n_ev);
+    evn[1] = n_keep ? atomicAdd(a.counters + 1, n_keep) : 0;
+    if (a.stats && n_keep) atomicAdd(a.stats, n_keep);
   }
   __syncthreads();
   const int base = evn[1];
-  for (int i = tid; i < n_ev; i += nth) {
-    if (base + i < a.ev_cap) a.events[base + i] = evb[i];
-    else send_to_fp64(a, (int64_t)(unsigned)evb[i].z, 3);
+  for (int i0 = 0; i0 < n_ev; i0 += nth) {
+    const int i = i0 + tid;
+    int4 e = make_int4(0, 0, 0, 0);
+    bool keep = i < n_ev;
+    if (keep) {
+      e = evb[i];
+      keep = !(ev_is_node(e.w) && e.y == 0);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    int slot = 0;
+    if (lane == 0 && bal) slot = atomicAdd(evn + 3, __popc(bal));
+    slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(bal & ((1u << lane) - 1u));
+    if (keep) {
+      if (base + slot < a.ev_cap) a.events[base + slot] = e;
+      else send_to_fp64(a, (int64_t)(unsigned)e.z, 3);
+    }
   }
 }
 
@@ -1592,6 +1668,8 @@ verify_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
 // ===========================================================================
 // fp32 re-trace of path p with lanes = rows; labw[pos] / prew[pos] (smem) for pos >= stop.
 // T / zrow may point to global or (staged) shared memory.
+// (An early exit at the first layer whose prefix exceeds the event bound was measured
+// slower: the exit test in every unrolled layer costs more than the layers it skips.)
 template <int N, int L>
 __device__ __forceinline__ void warp_retrace(const TabPtrs& T, const float4* zrow,
                                              const uint8_t* vlist, const TreeParams& tp, int p,
@@ -1842,7 +1920,7 @@ check_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
       const float4* zrow = S.z[warp][k];
       const uint8_t* vlist = a.lists + gv * tp.list_bytes;
       const float4 res = a.vres[gv];
-      const float lim = res.x + 2.f * ped_tol(res.x, res.w, N);
+      const float lim = node_lim(res, N);
       if (ev_is_node(e4.w)) {
         // every marked layer's prefix is >= evp: nothing can compete, no re-trace
         if (ev_node_evp(e4.w) <= lim) {
@@ -1851,8 +1929,11 @@ check_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
           warp_retrace<N, L>(T, zrow, vlist, tp, e4.x, lowest, lab, pre);
           bool zdone = false;
           double zr = 0.0, zi = 0.0;
-          for (int pos = N - 1; pos >= lowest; --pos) {
-            if (!((mask >> pos) & 1u) || pre[pos] > lim) continue;
+          // marked layers from the top down; prefixes only grow on the way down
+          for (unsigned mm = mask; mm;) {
+            const int pos = 31 - __clz(mm);
+            mm &= ~(1u << pos);
+            if (pre[pos] > lim) break;
             if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
             if (!zdone) { warp_z_f64(a, tab, gv, N, zr, zi); zdone = true; }
             double cr, ci;
