@@ -662,45 +662,45 @@ __device__ __forceinline__ void select_nearest(float xl, float yl, int E, int th
     // 64-QAM, E > 4.  Row i of the merge (the x-axis order's i-th level) offers the sum
     // dx_i + dy_{w_i}; its KEY is that sum with the three low mantissa bits replaced by
     // i, so the frontier's minimum and its row come out of one min tree (FMNMX3) and a
-    // mask instead of a compare/select chain.  Keys, per-axis orders and column counters
-    // live in per-thread (transposed) shared memory, so every data-dependent access is
-    // one LDS / STS.  Keys are non-decreasing along a row, hence the picks are exactly
+    // mask instead of a compare/select chain.  Keys and per-axis distances live in
+    // per-thread (transposed) shared memory, so every data-dependent access is one
+    // conflict-free LDS / STS.  Keys are non-decreasing along a row, hence the picks are exactly
     // the E smallest cells in KEY order; that order differs from the exact one only
     // between sums closer than 8 ulp, and the returned kprev / knext are keys (within
     // 8 ulp below the sums): select_cut_slack() widens the cut guard accordingly, so a
     // cut that the truncation could have changed is always logged and re-selected in
     // fp64 by the check kernel.
-    __shared__ float sdx[L][128], sdy[L][128];
-    __shared__ float4 snk[2][128];
-    __shared__ uint8_t sox[L][128], soy[L][128], sw[L][128];
+    __shared__ float sdx[L][128], sdy[L][128], snk[L][128];
     const float BIG = 1e30f;
     auto mkkey = [](float v, unsigned row) {
       return __uint_as_float((__float_as_uint(v) & ~7u) | row);
     };
+    // level orders and the rows' column counters as 4-bit fields of three registers
+    // (byte arrays in shared memory cost 2-4-way bank conflicts per lookup)
+    unsigned oxp = 0u, oyp = 0u, swp = 0u;
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-      sdx[i][th] = dx[i]; sdy[i][th] = dy[i];
-      sox[i][th] = (uint8_t)ox[i]; soy[i][th] = (uint8_t)oy[i]; sw[i][th] = 0;
+      sdx[i][th] = dx[i];
+      sdy[i][th] = dy[i];
+      snk[i][th] = mkkey(dx[i] + dy[0], (unsigned)i);
+      oxp |= (unsigned)ox[i] << (4 * i);
+      oyp |= (unsigned)oy[i] << (4 * i);
     }
-    snk[0][th] = make_float4(mkkey(dx[0] + dy[0], 0u), mkkey(dx[1] + dy[0], 1u),
-                             mkkey(dx[2] + dy[0], 2u), mkkey(dx[3] + dy[0], 3u));
-    snk[1][th] = make_float4(mkkey(dx[4] + dy[0], 4u), mkkey(dx[5] + dy[0], 5u),
-                             mkkey(dx[6] + dy[0], 6u), mkkey(dx[7] + dy[0], 7u));
-    float* nkf = reinterpret_cast<float*>(&snk[0][th]);
 #pragma unroll
     for (int pick = 0; pick <= EMAX; ++pick) {
       if (pick > E) break;
-      const float4 ka = snk[0][th], kb = snk[1][th];
-      const float best = fminf(fminf(fminf(fminf(ka.x, ka.y), ka.z), fminf(fminf(ka.w, kb.x), kb.y)),
-                               fminf(kb.z, kb.w));
+      const float best =
+          fminf(fminf(fminf(fminf(snk[0][th], snk[1][th]), snk[2][th]),
+                      fminf(fminf(snk[3][th], snk[4][th]), snk[5][th])),
+                fminf(snk[6][th], snk[7][th]));
       if (pick < E) {
-        const int sel = (int)(__float_as_uint(best) & 7u);
-        const int col = sw[sel][th];
-        const unsigned b = ((unsigned)sox[sel][th] << 3) | (unsigned)soy[col][th];
-        const int cn = col + 1 < L ? col + 1 : L - 1;
-        const float nxt = (col + 1 < L) ? sdx[sel][th] + sdy[cn][th] : BIG;
-        nkf[(sel >> 2) * (128 * 4) + (sel & 3)] = mkkey(nxt, (unsigned)sel);
-        sw[sel][th] = (uint8_t)(col + 1);
+        const unsigned sel = __float_as_uint(best) & 7u;
+        const unsigned col = (swp >> (4u * sel)) & 15u;
+        const unsigned b = (((oxp >> (4u * sel)) & 7u) << 3) | ((oyp >> (4u * col)) & 7u);
+        const unsigned cn = col + 1u < (unsigned)L ? col + 1u : (unsigned)(L - 1);
+        const float nxt = (col + 1u < (unsigned)L) ? sdx[sel][th] + sdy[cn][th] : BIG;
+        snk[sel][th] = mkkey(nxt, sel);
+        swp += 1u << (4u * sel);
         words[pick >> 2] |= b << (8 * (pick & 3));
         kprev = best;
       } else {
@@ -900,8 +900,11 @@ __device__ __forceinline__ constexpr float select_cut_slack() {
   return (L == 8 && EMAX > 4) ? 64.f : 0.f;
 }
 
+#ifndef MPNL_SELECT_MINB
+#define MPNL_SELECT_MINB 1   // minimum CTAs per SM asked of the compiler (register cap)
+#endif
 template <int N, int L, int EMAX>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, MPNL_SELECT_MINB)
 select_kernel(const DetectArgs a, const TreeParams tp, int pos, int npar, int vblocks) {
   const int E = tp.e[pos];   // <= EMAX
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;

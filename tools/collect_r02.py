@@ -96,6 +96,16 @@ ncu("e_ncu_plan_C5", "ncu_plan_qr_reg_C5.txt",
     "ncu --set full --clock-control none, plan kernel on C5's 2,048 24x24 channels")
 ncu("e_ncu_soft_C2", "ncu_soft_llr_C2.txt",
     "ncu --set full --clock-control none, fp32 soft-output kernel on C2 (273 RB x 168 RE)")
+ncu("e_ncu_select_C5P1024", "ncu_select_C5P1024.txt",
+    "ncu --set full --clock-control none, 64-QAM partial-layer selection (E = 16) on C5P1024")
+ncu("e_ncu_check_C5P1024", "ncu_check_C5P1024.txt",
+    "ncu --set full --clock-control none, event checks on C5P1024")
+ncu("e_ncu_check_C5P16", "ncu_check_C5P16.txt",
+    "ncu --set full --clock-control none, event checks on C5P16")
+ncu("e_ncu_prep2_C5P16", "ncu_prep2_C5P16.txt",
+    "ncu --set full --clock-control none, fp64 rotation + guard bounds on C5 (344,064 vectors)")
+ncu("e_ncu_verify_C5P16", "ncu_verify_C5P16.txt",
+    "ncu --set full --clock-control none, winner re-trace on C5 (344,064 vectors)")
 
 # roofline.traffic of the headline config from this round's capture
 raw = G / "e_ncu_traverse_C5P1024_raw.csv"

@@ -24,3 +24,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 bash tools/prof_full.sh e_ncu_traverse_C5P1024 C5P1024 traverse_kernel
 bash tools/prof_full.sh e_ncu_plan_C5 C5P16 plan_qr_reg
 bash tools/prof_full.sh e_ncu_soft_C2 C2 soft_llr 0 soft
+bash tools/prof_full.sh e_ncu_select_C5P1024 C5P1024 select_kernel
+bash tools/prof_full.sh e_ncu_check_C5P1024 C5P1024 check_kernel
+bash tools/prof_full.sh e_ncu_prep2_C5P16 C5P16 prep2_kernel
+bash tools/prof_full.sh e_ncu_verify_C5P16 C5P16 verify_kernel
+bash tools/prof_full.sh e_ncu_check_C5P16 C5P16 check_kernel
+rm -f gpurun_out/e_ncu_*_sass.csv.bak
