@@ -280,7 +280,8 @@ __device__ __forceinline__ void guard_mark(float d, float th, unsigned bit, floa
 
 // K3 inner loop: NS independent paths.  Per path: PED, mask of layers whose
 // decision was within the bound, and a lower bound of the PED prefix at the
-// first such layer (the re-part partial sum, taken with a predicated min).
+// first such layer (Ped<>::bound: the prefix itself, or its real half in the packed
+// mode; taken with a predicated min).
 // Accumulators are per row (re, im) f32x2 registers; decided symbols are held
 // as NEGATED level indices g = -n (what the magic-number rounding yields for
 // free), so every product with g uses a negated table operand -- exact, hence
@@ -298,6 +299,41 @@ __device__ __forceinline__ void guard_mark(float d, float th, unsigned bit, floa
 #ifndef MPNL_QDESC
 #define MPNL_QDESC 1
 #endif
+// PED accumulation.  Scalar: one chain ped += er^2; ped += ei^2 -- the guard then sees the
+// FULL prefix of a marked decision, so far fewer non-competitive paths are logged as
+// events (C5/P1024: 1.8 -> 0.76 per vector, verify + checks 1,493 -> 996 us for +120 us
+// of traversal).  Packed: the (sum er^2, sum ei^2) pair of one FFMA2 per layer, whose real
+// half is the guard's prefix bound -- kept where events are rare anyway and the extra issue
+// slot per layer only costs (16-QAM / QPSK with N <= 16: C2 traversal 300 vs 305 us).
+// The choice is a function of (N, L) only, so every re-trace twin makes the same one.
+#ifndef MPNL_PED_SCALAR
+#define MPNL_PED_SCALAR 1
+#endif
+template <int N, int L>
+__host__ __device__ constexpr bool ped_scalar() {
+  return MPNL_PED_SCALAR && !(L <= 4 && N <= 16);
+}
+template <bool SCALAR>
+struct Ped;
+template <>
+struct Ped<true> {
+  typedef float T;
+  static __device__ __forceinline__ T zero() { return 0.f; }
+  static __device__ __forceinline__ T add(u64 e2, T p) {
+    const float er = lo32(e2), ei = hi32(e2);
+    return __fmaf_rn(ei, ei, __fmaf_rn(er, er, p));
+  }
+  static __device__ __forceinline__ float bound(T p) { return p; }   // <= the PED prefix
+  static __device__ __forceinline__ float value(T p) { return p; }
+};
+template <>
+struct Ped<false> {
+  typedef u64 T;
+  static __device__ __forceinline__ T zero() { return 0ull; }
+  static __device__ __forceinline__ T add(u64 e2, T p) { return ffma2(e2, e2, p); }
+  static __device__ __forceinline__ float bound(T p) { return lo32(p); }
+  static __device__ __forceinline__ float value(T p) { return lo32(p) + hi32(p); }
+};
 template <int N, int L, int NS, bool GUARD, bool LAB, bool SAMEV = false, bool SH = false>
 __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* __restrict__ zs,
                                                const float* __restrict__ thr,
@@ -312,7 +348,9 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
   constexpr int N4 = (N + 3) & ~3;
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
   const float INF = __int_as_float(0x7f800000);
-  u64 acc[NS][2 * NPP], ped2[NS];
+  u64 acc[NS][2 * NPP];
+  using PA = Ped<ped_scalar<N, L>()>;
+  typename PA::T ped2[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
 #pragma unroll
@@ -321,7 +359,7 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
       acc[s][2 * q] = pk2(z.x, z.y);
       acc[s][2 * q + 1] = pk2(z.z, z.w);
     }
-    ped2[s] = 0ull;
+    ped2[s] = PA::zero();
     evm[s] = 0u;
     evp[s] = INF;
   }
@@ -371,14 +409,14 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
         if (GUARD) {
           const u64 t2 = ffma2(s2, LM2, g2[s]);
           const float th = thr[(SAMEV ? 0 : vl[s]) * N4 + pos];
-          guard_mark(fmaxf(fabsf(lo32(t2)), fabsf(hi32(t2))), th, 1u << pos, lo32(ped2[s]),
+          guard_mark(fmaxf(fabsf(lo32(t2)), fabsf(hi32(t2))), th, 1u << pos, PA::bound(ped2[s]),
                      evm[s], evp[s]);
         }
       }
     }
     if (LAB) {
       lab[pos] = (int)(-lo32(g2[0])) * 8 + (int)(-hi32(g2[0]));
-      pre[pos] = lo32(ped2[0]) + hi32(ped2[0]);
+      pre[pos] = PA::value(ped2[0]);
       if (pos == stop) return;
     }
     constexpr bool SH2 = SH && NS == 2;
@@ -388,7 +426,7 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
     for (int s = 0; s < NS; ++s) {
       if (s >= ns) break;
       const u64 e2 = ffma2(pk2(-c2r, -c2r), g2[s], acc[s][pos]);   // c2r n + u
-      ped2[s] = ffma2(e2, e2, ped2[s]);
+      ped2[s] = PA::add(e2, ped2[s]);
     }
     // push this layer's symbols into the rows below: acc_k += r''_k,pos * s.
     // Row pairs are walked top-down so the row the next layer slices (pos - 1)
@@ -421,7 +459,7 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
     }
   }
 #pragma unroll
-  for (int s = 0; s < NS; ++s) ped[s] = lo32(ped2[s]) + hi32(ped2[s]);
+  for (int s = 0; s < NS; ++s) ped[s] = PA::value(ped2[s]);
 }
 
 // Single-path re-trace with the identical arithmetic: level indices lab[pos]
@@ -1686,7 +1724,8 @@ __device__ __forceinline__ void warp_retrace(const TabPtrs& T, const float4* zro
     ar = zf.x;
     ai = zf.y;
   }
-  u64 ped2 = 0ull;
+  using PA = Ped<ped_scalar<N, L>()>;
+  typename PA::T ped2 = PA::zero();
   const int top_lo = N - tp.n_top;
 #pragma unroll
   for (int pos = N - 1; pos >= 0; --pos) {
@@ -1709,13 +1748,13 @@ __device__ __forceinline__ void warp_retrace(const TabPtrs& T, const float4* zro
     const float ur = __shfl_sync(0xffffffffu, ar, pos), ui = __shfl_sync(0xffffffffu, ai, pos);
     if (lane == 0) {
       labw[pos] = (int)fr * 8 + (int)fi;
-      prew[pos] = lo32(ped2) + hi32(ped2);
+      prew[pos] = PA::value(ped2);
     }
     if (pos == stop) break;
     const float er = __fmaf_rn(ly.y, fr, ur);
     const float ei = __fmaf_rn(ly.y, fi, ui);
     const u64 e2 = pk2(er, ei);
-    ped2 = ffma2(e2, e2, ped2);
+    ped2 = PA::add(e2, ped2);
     if (lane < pos) {
       ar = __fmaf_rn(rr.x, fr, ar);
       ar = __fmaf_rn(rr.y, -fi, ar);
@@ -1755,6 +1794,55 @@ __device__ __forceinline__ void warp_z_f64(const DetectArgs& a, const float* tab
     zr = fma(q.x, yr, fma(-q.y, yi, zr));
     zi = fma(q.x, yi, fma(q.y, yr, zi));
   }
+}
+
+// One row of the fp64 rotation, z_k = (Q^H y)_k, with the M products spread over the
+// lanes (lane = receive row) and a butterfly sum: every lane gets the same value.  An
+// event check needs only the marked layer's row: one load round trip and ~45
+// instructions instead of the M sequential steps of warp_z_f64.
+__device__ __forceinline__ void warp_zrow_f64(const DetectArgs& a, const float* tab, int64_t gv,
+                                              int n, int k, double& zr, double& zi) {
+  const int lane = threadIdx.x & 31;
+  const int m = a.m;
+  const double2* qt = reinterpret_cast<const double2*>(tab + TableLayout(m, n).off_qh);
+  double sr = 0.0, si = 0.0;
+  for (int r = lane; r < m; r += 32) {
+    double yr, yi;
+    if (a.y_f64) {
+      const double2 v = reinterpret_cast<const double2*>(a.y)[gv * m + r];
+      yr = v.x; yi = v.y;
+    } else {
+      const float2 v = reinterpret_cast<const float2*>(a.y)[gv * m + r];
+      yr = v.x; yi = v.y;
+    }
+    const double2 q = qt[r * n + k];
+    sr = fma(q.x, yr, fma(-q.y, yi, sr));
+    si = fma(q.x, yi, fma(q.y, yr, si));
+  }
+  zr = warp_sum_d(sr);
+  zi = warp_sum_d(si);
+}
+
+// fp64 centre of layer pos for the path whose level indices above pos are labw (smem),
+// from that layer's rotated value (zp_r, zp_i) alone
+__device__ __forceinline__ void warp_centre_f64_row(const DetectArgs& a, int64_t c, int n, int L,
+                                                    int pos, const int* labw, double zp_r,
+                                                    double zp_i, double& cr, double& ci) {
+  const int lane = threadIdx.x & 31;
+  const double* R = reinterpret_cast<const double*>(a.r64 + (c * n + pos) * (int64_t)n);
+  double sr_ = 0.0, si_ = 0.0;
+  const int j = pos + 1 + lane;
+  if (j < n) {
+    const double sr = level_value_rt(labw[j] >> 3, L), si = level_value_rt(labw[j] & 7, L);
+    const double rr = R[2 * j], ri = R[2 * j + 1];
+    sr_ = rr * sr - ri * si;
+    si_ = rr * si + ri * sr;
+  }
+  sr_ = warp_sum_d(sr_);
+  si_ = warp_sum_d(si_);
+  const double rpp = R[2 * pos];
+  cr = (zp_r - sr_) / rpp;
+  ci = (zp_i - si_) / rpp;
 }
 
 // fp64 centre of layer pos for the path whose level indices above pos are labw
@@ -1930,17 +2018,15 @@ check_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
           const unsigned mask = (unsigned)e4.y;
           const int lowest = __ffs(mask) - 1;
           warp_retrace<N, L>(T, zrow, vlist, tp, e4.x, lowest, lab, pre);
-          bool zdone = false;
-          double zr = 0.0, zi = 0.0;
           // marked layers from the top down; prefixes only grow on the way down
           for (unsigned mm = mask; mm;) {
             const int pos = 31 - __clz(mm);
             mm &= ~(1u << pos);
             if (pre[pos] > lim) break;
             if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
-            if (!zdone) { warp_z_f64(a, tab, gv, N, zr, zi); zdone = true; }
-            double cr, ci;
-            warp_centre_f64(a, c, N, L, pos, lab, zr, zi, cr, ci);
+            double cr, ci, zpr, zpi;
+            warp_zrow_f64(a, tab, gv, N, pos, zpr, zpi);   // only this layer's row of Q^H y
+            warp_centre_f64_row(a, c, N, L, pos, lab, zpr, zpi, cr, ci);
             const int ir = nearest_level_f64(cr, L, nrm), ii = nearest_level_f64(ci, L, nrm);
             if (ir * 8 + ii != lab[pos]) {
               // the reference takes the other branch here.  Our fp32 path is then
@@ -1950,6 +2036,8 @@ check_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
               const int2 pth = a.vpath[gv];
               bool bad = e4.x == pth.x || e4.x == pth.y;
               if (!bad) {
+                double zr, zi;
+                warp_z_f64(a, tab, gv, N, zr, zi);   // the continuation needs every row
                 const double malt = warp_sic_f64(a, c, N, L, pos, lab, ir, ii, zr, zi);
                 bad = malt <= (double)lim;
               }
@@ -1964,9 +2052,9 @@ check_kernel(const DetectArgs a, const TreeParams tparam, int unused) {
         const float prefix = (pos < N - 1) ? pre[pos + 1] : 0.f;   // <= PED prefix at pos
         if (prefix <= lim) {
           if (a.stats && lane == 0) atomicAdd(a.stats + 1, 1);
-          double zr, zi, cr, ci;
-          warp_z_f64(a, tab, gv, N, zr, zi);
-          warp_centre_f64(a, c, N, L, pos, lab, zr, zi, cr, ci);
+          double zpr, zpi, cr, ci;
+          warp_zrow_f64(a, tab, gv, N, pos, zpr, zpi);
+          warp_centre_f64_row(a, c, N, L, pos, lab, zpr, zpi, cr, ci);
           if (lane == 0) {
             const int e = tp.e[pos];
             const unsigned long long m64 = nearest_set_f64(cr, ci, L, nrm, e);
