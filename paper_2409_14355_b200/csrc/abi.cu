@@ -407,6 +407,7 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
   } else {
     ea.list = a.fix_list;
     ea.count = a.counters;
+    ea.split = 4;     // a cluster of 4 CTAs per flagged vector (latency tail of the step)
     grid = 148 * 2;   // a handful of flagged vectors: few, long-lived CTAs
   }
   e = launch_exact(ea, tp, grid, st);

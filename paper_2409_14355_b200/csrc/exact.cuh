@@ -22,7 +22,11 @@
 //     ||y||^2 - ||z||^2 (M > N) minus nv ||x||^2 (augmented)      :484-486
 //   best = lexicographic (metric, labels[stream 0], labels[1], ...) :465-470
 //
-// One CTA per received vector (grid-stride over the task list):
+// One CTA per received vector (grid-stride over the task list) -- or, in fix-up mode
+// (ExactArgs::split > 1), one thread-block CLUSTER per vector: the few flagged vectors
+// are the latency tail of every step, so each CTA of the cluster takes a contiguous
+// range of the paths (and builds only the selection lists of those paths' parents), and
+// rank 0 folds the ranks' winners through distributed shared memory:
 //   1. R of the vector's channel -> shared memory; z = Q^H y in fp64;
 //   2. selection lists of the expanded layers, top-down, thread per
 //      (parent, point): rank of the point among the parent's Q children by
@@ -31,6 +35,7 @@
 //      registers;
 //   4. block tree-argmin on (metric, labels in stream order).
 #pragma once
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
 #include "exact_args.cuh"
@@ -166,10 +171,10 @@ static __device__ __noinline__ int ex_expanded_symbol(const TreeParams& tp, cons
 template <int N, int L, int EM>
 __device__ __noinline__ void ex_scan_lists(const TreeParams& tp, const ExLayout& lo,
                                            uint8_t* lists, const double2* Rs, const double2* zs,
-                                           int pos, int npar, int e) {
+                                           int pos, int par_lo, int par_hi, int e) {
   constexpr int Q = L * L;
   constexpr int h = (L == 2) ? 1 : (L == 4 ? 2 : 3);
-  for (int par = threadIdx.x; par < npar; par += EX_THREADS) {
+  for (int par = par_lo + threadIdx.x; par < par_hi; par += EX_THREADS) {
     const int p0 = par * tp.stride[pos + 1];
     double ur = zs[pos].x, ui = zs[pos].y;
     for (int j = N - 1; j > pos; --j) {
@@ -227,7 +232,11 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
   const int m = a.m;
   // fix-up mode usually has a handful of tasks: idle CTAs leave at once
   const int64_t ntask = a.list ? (int64_t)(*a.count) : a.n_tasks;
-  if ((int64_t)blockIdx.x >= ntask) return;
+  // cluster mode: CTA `part` of `S` works on the cluster's vector (all ranks leave together)
+  const int S = a.split > 1 ? a.split : 1;
+  const int part = S > 1 ? (int)(blockIdx.x % (unsigned)S) : 0;
+  const int64_t group = blockIdx.x / (unsigned)S, ngroups = gridDim.x / (unsigned)S;
+  if (group >= ntask) return;
   TreeParams& tp = *reinterpret_cast<TreeParams*>(exsm + lo.tp);
   double2* Rs = reinterpret_cast<double2*>(exsm + lo.r);
   double2* QHs = reinterpret_cast<double2*>(exsm + lo.qh);
@@ -248,8 +257,10 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
     for (int i = tid; i < (int)(sizeof(TreeParams) / 4); i += EX_THREADS) d[i] = s[i];
   }
   const int P = tparam.n_paths;
+  const int PP = (P + S - 1) / S;                       // this CTA's paths [pa, pb)
+  const int pa = min(P, part * PP), pb = min(P, pa + PP);
   int64_t cprev = -1;
-  for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+  for (int64_t task = group; task < ntask; task += ngroups) {
     const int64_t gv = a.list ? a.list[task] : task;
     const int64_t c = gv / a.V;
     const double2* QH = a.qh64 + c * (int64_t)N * m;
@@ -319,18 +330,21 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
         if (!lo.listed[pos]) continue;
         __syncthreads();
         const int e = tp.e[pos];
-        const int npar = P / tp.stride[pos + 1];
+        // parents of this CTA's paths only
+        const int spar = tp.stride[pos + 1];
+        const int par_lo = pa / spar, par_hi = pb > pa ? (pb - 1) / spar + 1 : par_lo;
+        const int npar = par_hi - par_lo;
         if (e <= 8 && npar * Q > 2 * EX_THREADS) {
           // many parents, short lists: thread per parent, one pass over the Q
           // points keeping the e smallest (distance, label) in registers --
           // O(Q) per parent instead of the O(Q^2) rank count below (same key)
-          if (e <= 2) ex_scan_lists<N, L, 2>(tp, lo, lists, Rs, zs, pos, npar, e);
-          else if (e <= 4) ex_scan_lists<N, L, 4>(tp, lo, lists, Rs, zs, pos, npar, e);
-          else ex_scan_lists<N, L, 8>(tp, lo, lists, Rs, zs, pos, npar, e);
+          if (e <= 2) ex_scan_lists<N, L, 2>(tp, lo, lists, Rs, zs, pos, par_lo, par_hi, e);
+          else if (e <= 4) ex_scan_lists<N, L, 4>(tp, lo, lists, Rs, zs, pos, par_lo, par_hi, e);
+          else ex_scan_lists<N, L, 8>(tp, lo, lists, Rs, zs, pos, par_lo, par_hi, e);
           continue;
         }
         for (int it = tid; it < npar * Q; it += EX_THREADS) {
-          const int par = it / Q, q = it % Q;
+          const int par = par_lo + it / Q, q = it % Q;
           const int p0 = par * tp.stride[pos + 1];
           double ur = zs[pos].x, ui = zs[pos].y;
           for (int j = N - 1; j > pos; --j) {
@@ -373,7 +387,7 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
     // (rolled loops, residuals in local memory: the kernel runs for a few
     // vectors, so its cold instruction fetch, not its arithmetic, sets the
     // latency -- keep the code small)
-    for (int p = tid; p < P; p += EX_THREADS) {
+    for (int p = pa + tid; p < pb; p += EX_THREADS) {
       double2 acc[N];
 #pragma unroll 1
       for (int k = 0; k < N; ++k) acc[k] = make_double2(0.0, 0.0);
@@ -454,6 +468,32 @@ exact_kernel_t(const ExactArgs a, const TreeParams tparam, const ExLayout lo) {
       }
       __syncthreads();
     }
+    if (S > 1) {
+      // fold the ranks' winners into rank 0 (same total order as the block argmin)
+      namespace cg = cooperative_groups;
+      cg::cluster_group cl = cg::this_cluster();
+      cl.sync();
+      if (part == 0 && tid == 0) {
+        for (int r = 1; r < S; ++r) {
+          const double* rm = cl.map_shared_rank(cm, r);
+          const int* rp = cl.map_shared_rank(cp, r);
+          const unsigned long long* rk = cl.map_shared_rank(ck, r);
+          unsigned long long ko[EX_KW], kt[EX_KW];
+#pragma unroll
+          for (int ww = 0; ww < EX_KW; ++ww) { ko[ww] = rk[ww]; kt[ww] = ck[ww]; }
+          const int po = rp[0];
+          const double mo = rm[0];
+          if (po != 0x7fffffff && (cp[0] == 0x7fffffff || ex_key_less(mo, ko, cm[0], kt))) {
+            cm[0] = mo;
+            cp[0] = po;
+#pragma unroll
+            for (int ww = 0; ww < EX_KW; ++ww) ck[ww] = ko[ww];
+          }
+        }
+      }
+      cl.sync();   // remote reads done before any rank reuses its slots
+      if (part != 0) continue;
+    }
     if (tid < N) {
       // winner label of stream `tid` from the key
       const unsigned long long kw = ck[tid / 10];   // the winner's words (thread 0's slot)
@@ -480,6 +520,21 @@ cudaError_t launch_exact_t(const ExactArgs& a, const TreeParams& tp, int grid, c
   const size_t smem = (size_t)lo.total;
   cudaFuncSetAttribute(exact_kernel_t<N, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
+  if (a.split > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(grid / a.split * a.split));
+    cfg.blockDim = dim3(EX_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)a.split;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, exact_kernel_t<N, L>, a, tp, lo);
+  }
   exact_kernel_t<N, L><<<grid, EX_THREADS, smem, st>>>(a, tp, lo);
   return cudaGetLastError();
 }

@@ -25,6 +25,8 @@ struct ExactArgs {
   double* full_metrics;    // (B, P) or null
   int64_t* full_best;      // (B,) or null
   int exact_order;         // 1: full layers in stable distance order too
+  int split;               // > 1: a thread-block cluster of `split` CTAs shares one vector
+                           // (its paths and their parents' lists are divided; fix-up mode)
 };
 
 }  // namespace mpnl

@@ -52,6 +52,24 @@ def test_shapes_vs_oracle(m, n, order, p):
     _check(h, y, nv, p, c, hard, metric)
 
 
+@pytest.mark.parametrize("n,p", [(6, 8), (6, 16), (6, 32), (6, 512), (6, 1024), (6, 2048),
+                                 (6, 96), (4, 8192), (20, 1024)])
+def test_64qam_partial_layer_selections(n, p):
+    """64-QAM trees whose partial layer takes E = 8 / 16 / 32 / 48 of the 64 points, at the
+    top or under a full top layer (and a three-layer tree): the key-ordered selection merge
+    (select_kernel, L = 8) and its widened cut guard, hard output and fp32 LLRs vs the oracle."""
+    det = _det()
+    rng = np.random.default_rng(7000 + 13 * n + p)
+    c, h, y, nv = _case(rng, 3, 32, n, n, 64, snr_db=20.0)
+    plan = det.mpnl_plan_batch(h, nv, p, c)
+    hard, metric = det.mpnl_detect_hard(plan, h, y, c)
+    _check(h, y, nv, p, c, hard, metric)
+    if p <= 1024:
+        llr = det.mpnl_detect_llrs(plan, h, y[:, :24].copy(), c, precision="fp32")
+        ref = det.mpnl_detect_llrs(plan, h, y[:, :24].copy(), c)
+        assert np.abs(llr - ref).max() <= 1e-3
+
+
 @pytest.mark.parametrize("n_ch,v,m,n,order,p", [(300, 1, 8, 8, 16, 32), (257, 3, 12, 12, 16, 64),
                                                 (70, 2, 24, 24, 64, 64), (40, 1, 32, 32, 16, 32),
                                                 (9, 1, 8, 8, 16, 32), (130, 5, 16, 16, 64, 16)])
