@@ -366,15 +366,8 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     if (items > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "too many work items");
     // channels with fewer than two path batches per warp: a warp per channel
     a.wpc = ((v_per_ch + nvi - 1) / nvi) * (int64_t)bpv < 2 * warps && n_ch >= 2 * warps ? 1 : 0;
-    // several batches per vector: a per-CTA table of every batch's expanded-layer symbols
-    // replaces the per-path mixed-radix decoding (up to 8 KB; list positions fit 16 bits)
-    a.xtn = 0;
-    if (bpv > 1 && !a.wpc && tp.n_top >= 1 && tp.list_bytes < 65536) {
-      const int64_t ent = (int64_t)bpv * S * std::min(tp.n_top, std::min(n, MPNL_XMAX));
-      if (2 * ent <= 8192) a.xtn = (int)ent;
-    }
     if (stage == 2) {
-      const TravSmem so(m, n, warps, nvi, tp.list_bytes, a.wpc != 0, a.xtn);
+      const TravSmem so(m, n, warps, nvi, tp.list_bytes, a.wpc != 0);
       e = launch_fast(n, L, 1, a, tp, 0, threads, so.total_bytes, (int)items, st);
       if (e != cudaSuccess) return cuda_fail(e, "traverse kernel");
     } else {

@@ -77,7 +77,6 @@ struct DetectArgs {
   int metric_offset;        // 1 when M > N: add ||y||^2 - ||z||^2
   float guard_scale;        // scales the fp32 error bound (1 = rigorous)
   int wpc;                  // traversal: 1 = a warp per channel (few vectors per channel)
-  int xtn;                  // traversal: entries of the per-CTA batch symbol table (0 = off)
   SoftArgs soft;            // soft_llr_kernel only
 };
 
@@ -344,9 +343,7 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
                                                const int (&p)[NS], float (&ped)[NS],
                                                unsigned (&evm)[NS], float (&evp)[NS],
                                                int* lab = nullptr, float* pre = nullptr,
-                                               int stop = -1, const u64* xs = nullptr,
-                                               const uint16_t* xt = nullptr,
-                                               const u64* symt = nullptr) {
+                                               int stop = -1, const u64* xs = nullptr) {
   constexpr int NPP = (N + 1) / 2;
   constexpr int N4 = (N + 3) & ~3;
   constexpr int XM = N < MPNL_XMAX ? N : MPNL_XMAX;
@@ -388,23 +385,6 @@ __device__ __forceinline__ void traverse_paths(const TabPtrs& T, const float4* _
           } else {
             const unsigned b = lists[(SAMEV ? 0 : (int)gvl[s]) * list_bytes + (int)(unsigned)x];
             // -(float)k for k < 8 without I2F: MAGIC - (MAGIC + k), one FADD2
-            g2[s] = fsub2(pk2(MPNL_MAGIC, MPNL_MAGIC),
-                          pk2(__uint_as_float(0x4B400000u | (b >> 3)),
-                              __uint_as_float(0x4B400000u | (b & 7u))));
-          }
-        }
-      } else if (xt != nullptr) {
-        // multi-batch trees: this batch's digits / list positions from the CTA's table
-        // (built once per CTA: no per-path mixed-radix divisions), full layers' negated
-        // level pairs from a 64-entry table
-        const bool full = tp.e[pos] == L * L;
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          const unsigned v = xt[((N - 1 - pos) * NS + s) * 32];
-          if (full) {
-            g2[s] = symt[v];
-          } else {
-            const unsigned b = lists[(SAMEV ? 0 : (int)gvl[s]) * list_bytes + (int)v];
             g2[s] = fsub2(pk2(MPNL_MAGIC, MPNL_MAGIC),
                           pk2(__uint_as_float(0x4B400000u | (b >> 3)),
                               __uint_as_float(0x4B400000u | (b & 7u))));
@@ -1195,13 +1175,11 @@ prep2_kernel(const DetectArgs a, const TreeParams tp, int chunks, int pos_sel) {
 #define MPNL_CHUNK_V 8          // vectors per warp chunk (one bulk-copy group)
 #endif
 struct TravSmem {
-  int tpo, tab, wbuf, bufsz, zs, thr, lst, eac, mbar, xs, xt, sym, ev, evn, total_bytes;   // floats / bytes
+  int tpo, tab, wbuf, bufsz, zs, thr, lst, eac, mbar, xs, ev, evn, total_bytes;   // floats / bytes
   int ck, cv;   // items and vectors per chunk
   int tab0, tabn;   // staged slice of the channel's table blob (per-layer float4 + r'' columns)
   // wpc: warp-per-channel mode, every warp stages its own channel's table slice
-  // xtn: entries of the batch symbol table (multi-batch trees; 0 = none)
-  __host__ __device__ TravSmem(int m, int n, int warps, int nvi, int list_bytes, bool wpc = false,
-                               int xtn = 0) {
+  __host__ __device__ TravSmem(int m, int n, int warps, int nvi, int list_bytes, bool wpc = false) {
     TableLayout tl(m, n);
     const int npp = (n + 1) / 2, n4 = (n + 3) & ~3;
     // chunk: up to MPNL_CHUNK_V vectors, at most ~2 KB per buffer (large
@@ -1229,8 +1207,6 @@ struct TravSmem {
     wbuf = o; o += warps * 2 * bufsz;
     mbar = o; o += warps * 2 * 2;                  // u64 mbarrier per warp buffer
     xs = o; o += 2 * MPNL_XMAX * MPNL_PT_SMALL * MPNL_XS_STRIDE;   // u64 per-thread symbols
-    xt = o; o += TableLayout::up4((xtn + 1) / 2);  // u16 per (batch, expanded layer, path slot)
-    sym = o; o += xtn ? 2 * 64 : 0;                // u64 negated level pair per full-layer digit
     ev = o; o += 4 * TRAV_EV_CAP;                  // int4 event buffer
     evn = o; o += 4;
     total_bytes = o * 4;
@@ -1302,7 +1278,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
   // (a template parameter: the CTA-mode instances keep their instruction schedule)
   constexpr bool wpc = WPC;
   static_assert(!WPC || (!SH && !ONEB), "warp-per-channel mode: plain or VPI instances");
-  const TravSmem so(a.m, N, nw, nvi, tparam.list_bytes, wpc, a.xtn);
+  const TravSmem so(a.m, N, nw, nvi, tparam.list_bytes, wpc);
   const TableLayout tl(a.m, N);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const float INF = __int_as_float(0x7f800000);
@@ -1356,31 +1332,6 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         xs[(j * PT + t) * MPNL_XS_STRIDE] = x;
       }
     }
-  }
-  // several batches per vector: the expanded layers' digits (full layer) / list positions
-  // (partial layer) of every (batch, path slot), [batch][layer][slot t][lane]
-  const bool use_xt = !use_xs && a.xtn > 0;
-  const int xt_nt = tparam.n_top < (N < MPNL_XMAX ? N : MPNL_XMAX) ? tparam.n_top
-                                                                   : (N < MPNL_XMAX ? N : MPNL_XMAX);
-  uint16_t* xtab = reinterpret_cast<uint16_t*>(sm + so.xt);
-  u64* symt = reinterpret_cast<u64*>(sm + so.sym);
-  if (use_xt) {
-    for (int i = tid; i < a.xtn; i += nth) {
-      const int ln = i & 31;
-      int r = i >> 5;
-      const int t = r % PT;
-      r /= PT;
-      const int j = r % xt_nt, b = r / xt_nt;
-      const int s = SH ? 2 * ln + t : t * 32 + ln;
-      const int p = b * S + s, pos = N - 1 - j;
-      unsigned v = 0u;
-      if (p < P) {
-        const int e = tparam.e[pos], d = p / tparam.stride[pos];
-        v = (e == L * L) ? (unsigned)(d % e) : (unsigned)(tparam.list_off[pos] + d);
-      }
-      xtab[i] = (uint16_t)v;
-    }
-    for (int i = tid; i < L * L; i += nth) symt[i] = pk2(-(float)(i / L), -(float)(i % L));
   }
   const int V = (int)a.V;
   const int ipc = (V + nvi - 1) / nvi;                      // items per channel
@@ -1496,10 +1447,7 @@ traverse_kernel(const DetectArgs a, const TreeParams tparam) {
         unsigned evm[PT];
         traverse_paths<N, L, PT, true, false, !VPI, SH>(T, zs, thr, lch, tp, lbytes, vl, gvl, pp, ped,
                                                     evm, evp, nullptr, nullptr, -1,
-                                                    use_xs ? xs : nullptr,
-                                                    use_xt ? xtab + b * (xt_nt * PT * 32) + lane
-                                                           : nullptr,
-                                                    symt);
+                                                    use_xs ? xs : nullptr);
         if (ONEB) {   // the lane's two paths, ordered (path 2l < 2l + 1)
           const bool sw = ped[1] < ped[0];
           run.m1 = sw ? ped[1] : ped[0];
