@@ -334,7 +334,10 @@ int mpnl_detect_hard_stage(int stage, const int32_t* perm, const void* r64, cons
     }
     // one thread per vector for large batches; 4 (rows and parents split) when
     // a thread per vector would leave the SMs short of warps
-    const int tpv = B >= 148 * 128 * 8 ? 1 : 4;
+    // (with no fused selection to divide, one thread per vector already pays at two CTAs per
+    // SM: C4's 45,864 vectors 72 -> 51 us, C5 at 256-512 RBs -5% of the step; with 64 fused
+    // parent selections per vector -- C3 -- four threads stay better until the SMs are full)
+    const int tpv = B >= 148 * 128 * (fused < 0 ? 2 : 8) ? 1 : 4;
     const int64_t pch = (v_per_ch + 128 / tpv - 1) / (128 / tpv);
     if (n_ch * pch > 0x7fffffffLL) return fail(MPNL_EUNSUPPORTED, "grid too large");
     if (16 * (m + 2) * n + 128 * 16 * (m | 1) > 200 * 1024)
