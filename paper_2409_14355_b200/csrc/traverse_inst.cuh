@@ -71,7 +71,10 @@ cudaError_t launch_fast_one(int kind, const DetectArgs& a, const TreeParams& tp,
       }();
       const long long cap = (long long)std::max(nb, 1) * sms;
       const long long work = (long long)extra * std::max(a.bpv, 1);
+      // (very long grids -- C5 at P >= 256: over 1,000 path batches per resident warp --
+      // gain another 0.5% from six waves; C2 / C3 / C4 are best at four or fewer)
       int waves = work >= 64LL * cap * (threads / 32) ? MPNL_TRAV_WAVES : 1;
+      if (work >= 1024LL * cap * (threads / 32)) waves = MPNL_TRAV_WAVES + MPNL_TRAV_WAVES / 2;
       if (env_waves > 0) waves = env_waves;
       grid = (unsigned)std::min<long long>(cap * waves, (long long)extra);
       if (a.wpc)   // a warp per channel: one wave of CTAs, never more warps than channels
