@@ -70,6 +70,28 @@ def test_64qam_partial_layer_selections(n, p):
         assert np.abs(llr - ref).max() <= 1e-3
 
 
+@pytest.mark.parametrize("n,order,p", [(8, 16, 256), (6, 64, 1024), (4, 4, 16), (12, 16, 64),
+                                       (8, 16, 32)])
+def test_all_zero_observations_tie_rules(n, order, p):
+    """y = 0: every SIC decision sits exactly on a slicing boundary and every path ties with
+    its negation, so the result is decided by the reference's tie rules alone (stable argsort
+    of equal distances, lexsort on (metric, labels)).  No tie exemption here: every vector
+    goes through the guard, the event checks and the fp64 fix-up (a cluster of CTAs per
+    vector for the trees of >= 256 paths) and must equal the oracle's labels exactly."""
+    det = _det()
+    rng = np.random.default_rng(n * 7 + p)
+    c = constellation_for(order)
+    h = ((rng.standard_normal((3, n, n)) + 1j * rng.standard_normal((3, n, n)))
+         / np.sqrt(2)).astype(np.complex64)
+    y = np.zeros((3, 8, n), np.complex64)
+    plan = det.mpnl_plan_batch(h, 0.1, p, c)
+    hard, metric, flags = det.mpnl_detect_hard(plan, h, y, c, return_flags=True)
+    ref, m1, _ = orc.detect_rb(h, y, 0.1, p, c.order, c.points)
+    assert np.array_equal(np.asarray(hard), ref)
+    assert np.allclose(np.asarray(metric, dtype=np.float64), m1, rtol=METRIC_REL)
+    assert np.asarray(flags).any()   # the fp64 fix-up did run
+
+
 @pytest.mark.parametrize("n_ch,v,m,n,order,p", [(300, 1, 8, 8, 16, 32), (257, 3, 12, 12, 16, 64),
                                                 (70, 2, 24, 24, 64, 64), (40, 1, 32, 32, 16, 32),
                                                 (9, 1, 8, 8, 16, 32), (130, 5, 16, 16, 64, 16)])
