@@ -70,6 +70,41 @@ def test_64qam_partial_layer_selections(n, p):
         assert np.abs(llr - ref).max() <= 1e-3
 
 
+@pytest.mark.parametrize("n,order,p", [(6, 64, 1024), (8, 16, 256), (6, 64, 16), (12, 16, 64),
+                                       (24, 64, 64)])
+@pytest.mark.parametrize("kind,metric_rel", [("y*30", 1e-4), ("y*1000", 1e-4), ("y*1e-4", 1e-4),
+                                             ("cols40dB", 1e-4), ("cols80dB", 1e-3)])
+def test_out_of_range_inputs(n, order, p, kind, metric_rel):
+    """Observations far outside the constellation (every slicing saturates, selection centres
+    far off the grid), tiny observations, and channels whose columns differ by 40 / 80 dB in
+    power: labels equal the oracle's (tie exemption as everywhere).  The fp32 metric keeps the
+    1e-4 bound up to 40 dB of column range; at 80 dB the fp32 rounding of the rotated
+    observation is 3e-4 of the (then tiny) residual -- a documented limit."""
+    det = _det()
+    rng = np.random.default_rng(n * 7 + p)
+    c = constellation_for(order)
+    h = ((rng.standard_normal((3, n, n)) + 1j * rng.standard_normal((3, n, n)))
+         / np.sqrt(2)).astype(np.complex64)
+    if kind == "cols40dB":
+        h = (h * np.asarray([1, 0.1, 10] * 8, np.float32)[None, None, :n]).astype(np.complex64)
+    if kind == "cols80dB":
+        h = (h * np.asarray([1, 1e-2, 1e2] * 8, np.float32)[None, None, :n]).astype(np.complex64)
+    ysc = {"y*30": 30.0, "y*1000": 1000.0, "y*1e-4": 1e-4}.get(kind, 1.0)
+    lab = rng.integers(0, order, (3, 24, n))
+    nv = 0.05
+    noise = np.sqrt(nv / 2) * (rng.standard_normal((3, 24, n)) + 1j * rng.standard_normal((3, 24, n)))
+    y = ((np.einsum("cmn,cvn->cvm", h.astype(complex), c.points[lab]) + noise) * ysc
+         ).astype(np.complex64)
+    plan = det.mpnl_plan_batch(h, nv, p, c)
+    hard, metric = det.mpnl_detect_hard(plan, h, y, c)
+    ref, m1, m2 = orc.detect_rb(h, y, nv, p, c.order, c.points)
+    exempt = (m2 - m1) <= TIE_REL * m1
+    bad = np.any(np.asarray(hard) != ref, axis=-1) & ~exempt
+    assert not bad.any(), f"{int(bad.sum())} vectors differ"
+    rel = np.abs(np.asarray(metric, dtype=np.float64) - m1) / np.maximum(m1, 1e-300)
+    assert np.all(rel[~exempt] <= metric_rel)
+
+
 @pytest.mark.parametrize("n,order,p", [(8, 16, 256), (6, 64, 1024), (4, 4, 16), (12, 16, 64),
                                        (8, 16, 32)])
 def test_all_zero_observations_tie_rules(n, order, p):
